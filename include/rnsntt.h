@@ -1,0 +1,139 @@
+/*
+ * rnsntt.h -- C ABI of the B200-native batched negacyclic NTT library
+ * (librnsntt.so, package paper_2410_05934_b200).
+ *
+ * The operation is Eq. 1 of arxiv 2410.05934:
+ *
+ *     c = INTT^{GS,psi^-1}_{bo->no}( NTT^{CT,psi}_{no->bo}(a) (.) NTT^{CT,psi}_{no->bo}(b) )
+ *
+ * over R_q = Z_q[x]/(x^N + 1), applied independently to every RNS
+ * limb q_l of every polynomial of a batch (RNS representation of the big
+ * modulus Q; CMux-level batching of TFHE polynomials).
+ *
+ * Conventions fixed by DESIGN.md "Readings":
+ *   C1  psi_l defaults to the numerically smallest primitive 2N-th root mod q_l.
+ *   C3  forward output slot k holds the evaluation of a at psi^{2 brv(k) + 1}
+ *       ("no -> bo"); the inverse takes that order back to natural.
+ *   C4  the inverse includes the final N^{-1} scaling, so
+ *       INTT(NTT(a)) = a.
+ *   C5  residues are canonical, 0 <= r < q_l, on input and on output.
+ *   C10 data layout is [batch][n_limbs][N] uint64 (limb-major, each limb is a
+ *       contiguous 8N-byte vector).
+ *
+ * Ownership: a plan owns its device tables (allocated on the device current at
+ * rnt_plan_create); the caller owns every data buffer and every stream.
+ * Errors: argument and plan errors are returned synchronously, before any
+ * launch, and nothing is launched.  Asynchronous device faults surface as
+ * RNT_E_CUDA from a later call.  No call performs a host synchronisation.
+ * No exception crosses this boundary.
+ * Thread safety: a plan is immutable after creation and may be used from
+ * several host threads and streams concurrently.
+ */
+#ifndef RNSNTT_H
+#define RNSNTT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rnt_plan_s* rnt_plan;
+
+typedef enum {
+  RNT_OK = 0,
+  RNT_E_INVALID_ARG = 1,   /* null pointer, n_limbs == 0, size overflow, pointer not 16-byte aligned */
+  RNT_E_UNSUPPORTED_N = 2, /* log2n outside [RNT_MIN_LOG2N, RNT_MAX_LOG2N] */
+  RNT_E_MODULUS = 3,       /* q not prime, q != 1 mod 2N, q >= 2^62, or duplicate moduli */
+  RNT_E_ROOT = 4,          /* caller-supplied psi is not a primitive 2N-th root of unity mod q */
+  RNT_E_PLAN_MISMATCH = 5, /* current device differs from the plan's device */
+  RNT_E_CUDA = 6,          /* a CUDA runtime call failed; see rnt_last_cuda_error() */
+  RNT_E_OOM = 7            /* device or host allocation failed */
+} rnt_status;
+
+#define RNT_MIN_LOG2N 4u
+#define RNT_MAX_LOG2N 16u
+#define RNT_MAX_LIMBS 1024u
+
+/* Build a plan for N = 2^log2n and n_limbs moduli (host array moduli[n_limbs]).
+ * psi: host array [n_limbs] of primitive 2N-th roots, or NULL for reading C1.
+ * device: CUDA device ordinal that will own the tables (and run the kernels).
+ * Validates every modulus (prime, q = 1 mod 2N, q < 2^62, pairwise distinct)
+ * and every psi (psi^N = -1 mod q); computes the bit-reversed twiddle
+ * tables of psi and psi^{-1} with their Shoup companions, N^{-1} and the
+ * Montgomery constants, and uploads them.  Synchronous; not on the hot path. */
+rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs,
+                           const uint64_t* moduli, const uint64_t* psi, int device);
+
+/* Free the plan's device tables.  The caller must ensure no work using the
+ * plan is still in flight.  NULL is accepted (no-op). */
+rnt_status rnt_plan_destroy(rnt_plan p);
+
+/* Read back N, the limb count and (optionally, host array [n_limbs]) the psi
+ * values the plan uses.  Any output pointer may be NULL. */
+rnt_status rnt_plan_query(rnt_plan p, uint32_t* log2n, uint32_t* n_limbs, uint64_t* psi_out,
+                          int* device);
+
+/* Forward negacyclic NTT, NTT^{CT,psi}_{no->bo} of Eq. 1, of
+ * every limb of `batch` polynomials.  in/out: device pointers to
+ * [batch][n_limbs][N] uint64, 16-byte aligned.  out == in (in place) is
+ * allowed; any other overlap is undefined.  batch == 0 is a no-op.
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream). */
+rnt_status rnt_ntt_forward(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch,
+                           void* stream);
+
+/* Inverse negacyclic NTT, INTT^{GS,psi^-1}_{bo->no} of Eq. 1
+ * including the N^{-1} scaling.  Same argument rules as forward. */
+rnt_status rnt_ntt_inverse(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch,
+                           void* stream);
+
+/* NTT-domain pointwise product, the (.) of Eq. 1 (ModMul):
+ * c[b][l][k] = a_hat[b][l][k] * b_hat[b'][l][k] mod q_l, with b' = b, or
+ * b' = 0 when b_broadcast != 0 (b_hat is then [n_limbs][N], reused for every
+ * polynomial).  c may alias a_hat.  Device pointers, 16-byte aligned. */
+rnt_status rnt_pointwise_mul(rnt_plan p, uint64_t* c, const uint64_t* a_hat,
+                             const uint64_t* b_hat, uint32_t batch, int b_broadcast,
+                             void* stream);
+
+/* Negacyclic product c = a * b mod (x^N + 1) per limb by Eq. 1:
+ *   b_is_eval == 0:  c = INTT(NTT(a) (.) NTT(b)), b in coefficient form;
+ *   b_is_eval != 0:  c = INTT(NTT(a) (.) b), b already in NTT form (e.g. a
+ *                    key held in evaluation form).
+ * b may be broadcast ([n_limbs][N]) with b_broadcast != 0.  c may alias a;
+ * c must not alias b.  Fused kernels: the NTT-domain intermediate never
+ * leaves the SM for N <= 2^10 and never leaves the row tile for N >= 2^11. */
+rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_t* b,
+                       uint32_t batch, int b_is_eval, int b_broadcast, void* stream);
+
+/* Operation codes for rnt_execute_host. */
+typedef enum {
+  RNT_OP_FORWARD = 0,
+  RNT_OP_INVERSE = 1,
+  RNT_OP_POLYMUL_EVAL = 2, /* c = INTT(NTT(a) (.) b_dev), b_dev device-resident NTT-form operand */
+  RNT_OP_POLYMUL = 3       /* c = INTT(NTT(a) (.) NTT(b_dev)), b_dev device-resident coefficients */
+} rnt_op;
+
+/* End-to-end convenience over HOST buffers: copies in_host (pinned host
+ * memory recommended) to the device workspace dev_ws, runs `op`, and copies
+ * the result to out_host, all asynchronously on `stream`.  dev_ws: caller-
+ * owned device buffer of batch*n_limbs*N uint64.  b_dev: device operand for
+ * the polymul ops (ignored otherwise).  The caller synchronises the stream
+ * before reading out_host. */
+rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uint64_t* in_host,
+                            uint64_t* dev_ws, const uint64_t* b_dev, uint32_t batch,
+                            int b_broadcast, void* stream);
+
+/* Human-readable name of a status code (static storage). */
+const char* rnt_status_string(rnt_status s);
+
+/* The cudaError_t of the last RNT_E_CUDA / RNT_E_OOM returned on this host thread. */
+int rnt_last_cuda_error(void);
+
+/* Number of kernels the library launched since process start (all threads);
+ * used by bench.py to report gpu_launches. */
+uint64_t rnt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNSNTT_H */

@@ -1,0 +1,326 @@
+/*
+ * ntt_oracle.c -- plain, slow, obviously-correct CPU oracle for the batched
+ * negacyclic NTT / INTT / pointwise-modmul path of arxiv 2410.05934
+ * ("Chameleon"), section II.D, Eq. 1.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (the package
+ * paper_2410_05934_b200/, its CUDA kernels or its C ABI) may include, link or
+ * call this file.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs use it.  It shares no code, header,
+ * table or constant generator with the CUDA path.
+ *
+ * Arithmetic: every modular product is the exact 128-bit product reduced with
+ * the C '%' operator (no Barrett, Shoup or Montgomery), every sum is reduced
+ * with '%'.  Residues are canonical in [0, q).
+ *
+ * Citations (P:n = PAPER.md line n, S:n = SPEC.md line n):
+ *   - ring and product c(x) = a(x) b(x) mod (x^N + 1) ............ P:194
+ *   - NTT^{CT,psi}_{no->bo}, INTT^{GS,psi^-1}_{bo->no}, Eq. 1 ..... P:205-213
+ *   - psi: primitive 2N-th root, psi^{2N}=1, psi^i != 1 (i<2N) .... P:213
+ *   - INTT includes the final N^{-1} scaling (reading C4) ......... S:165-167
+ *   - choice of psi (smallest primitive root, reading C1) and of
+ *     the primes (L largest q < 2^60, q = 1 mod 2N, reading C2) ... DESIGN.md
+ */
+#include "ntt_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+/* ---------------------------------------------------------------- scalars */
+
+uint64_t or_mulmod(uint64_t a, uint64_t b, uint64_t q) {
+  return (uint64_t)(((u128)a * (u128)b) % (u128)q);
+}
+
+uint64_t or_addmod(uint64_t a, uint64_t b, uint64_t q) {
+  return (uint64_t)(((u128)a + (u128)b) % (u128)q);
+}
+
+uint64_t or_submod(uint64_t a, uint64_t b, uint64_t q) {
+  return (uint64_t)(((u128)a + (u128)q - (u128)b) % (u128)q);
+}
+
+uint64_t or_powmod(uint64_t base, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q, b = base % q;
+  while (e) {
+    if (e & 1) r = or_mulmod(r, b, q);
+    b = or_mulmod(b, b, q);
+    e >>= 1;
+  }
+  return r;
+}
+
+/* Deterministic Miller-Rabin; bases 2..37 are exact for all n < 2^64. */
+int or_is_prime(uint64_t n) {
+  static const uint64_t bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return 0;
+  for (int i = 0; i < 12; ++i) {
+    if (n == bases[i]) return 1;
+    if (n % bases[i] == 0) return 0;
+  }
+  uint64_t d = n - 1;
+  int s = 0;
+  while ((d & 1) == 0) { d >>= 1; ++s; }
+  for (int i = 0; i < 12; ++i) {
+    uint64_t x = or_powmod(bases[i], d, n);
+    if (x == 1 || x == n - 1) continue;
+    int composite = 1;
+    for (int r = 1; r < s; ++r) {
+      x = or_mulmod(x, x, n);
+      if (x == n - 1) { composite = 0; break; }
+    }
+    if (composite) return 0;
+  }
+  return 1;
+}
+
+/* bit reversal of the low logn bits of i */
+uint32_t or_brv(uint32_t i, uint32_t logn) {
+  uint32_t r = 0;
+  for (uint32_t b = 0; b < logn; ++b) r |= ((i >> b) & 1u) << (logn - 1 - b);
+  return r;
+}
+
+/* psi is a primitive 2N-th root of unity mod q: psi^{2N} = 1 and
+ * psi^i != 1 for 0 < i < 2N.  For N a power of two this is psi^N = q - 1. */
+int or_is_primitive_2n_root(uint64_t psi, uint64_t q, uint32_t logn) {
+  uint64_t n = (uint64_t)1 << logn;
+  if (psi == 0 || psi >= q) return 0;
+  return or_powmod(psi, n, q) == q - 1;
+}
+
+/* Reading C1: the numerically smallest primitive 2N-th root of unity.
+ * Step 1: find any primitive root r = x^{(q-1)/2N} with r^N = -1.
+ * Step 2: the primitive 2N-th roots are exactly r^{2t+1}, t in [0,N);
+ *         enumerate them by repeated multiplication with r^2, keep the min. */
+uint64_t or_min_psi(uint64_t q, uint32_t logn) {
+  uint64_t n = (uint64_t)1 << logn, two_n = n << 1;
+  if ((q - 1) % two_n != 0) return 0;
+  uint64_t r = 0;
+  for (uint64_t x = 2; x < q; ++x) {
+    uint64_t c = or_powmod(x, (q - 1) / two_n, q);
+    if (or_powmod(c, n, q) == q - 1) { r = c; break; }
+  }
+  if (r == 0) return 0;
+  uint64_t r2 = or_mulmod(r, r, q), cur = r, best = r;
+  for (uint64_t t = 0; t < n; ++t) {
+    if (cur < best) best = cur;
+    cur = or_mulmod(cur, r2, q);
+  }
+  return best;
+}
+
+/* Reading C2: the L largest primes q < 2^60 with q = 1 (mod 2N), descending. */
+int or_primes(uint32_t logn, uint32_t count, uint64_t* out) {
+  uint64_t two_n = (uint64_t)2 << logn;
+  uint64_t k = (((uint64_t)1 << 60) - 1) / two_n; /* largest k with k*2N+1 < 2^60 */
+  uint32_t found = 0;
+  while (found < count && k > 0) {
+    uint64_t q = k * two_n + 1;
+    if (q < ((uint64_t)1 << 60) && or_is_prime(q)) out[found++] = q;
+    --k;
+  }
+  return found == count ? 0 : -1;
+}
+
+/* ---------------------------------------------------------------- tables */
+
+/* fwd[i] = psi^{brv(i)}, inv[i] = (psi^{-1})^{brv(i)}, ninv = N^{-1} mod q
+ * (the twiddle tables the Longa-Naehrig CT/GS loops below index). */
+void or_tables(uint64_t q, uint64_t psi, uint32_t logn, uint64_t* fwd, uint64_t* inv,
+               uint64_t* ninv) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t psi_inv = or_powmod(psi, q - 2, q); /* Fermat: q prime */
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t e = or_brv((uint32_t)i, logn);
+    fwd[i] = or_powmod(psi, e, q);
+    inv[i] = or_powmod(psi_inv, e, q);
+  }
+  *ninv = or_powmod(n % q, q - 2, q);
+}
+
+/* ------------------------------------------------------------- transforms */
+
+/* NTT^{CT,psi}_{no->bo} (Eq. 1): Cooley-Tukey butterflies,
+ * natural-order input, bit-reversed-order output, in place. */
+void or_ntt_fwd(uint64_t* a, uint32_t logn, uint64_t q, const uint64_t* fwd) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t t = n;
+  for (uint64_t m = 1; m < n; m <<= 1) {
+    t >>= 1;
+    for (uint64_t i = 0; i < m; ++i) {
+      uint64_t S = fwd[m + i];
+      uint64_t j1 = 2 * i * t;
+      for (uint64_t j = j1; j < j1 + t; ++j) {
+        uint64_t U = a[j];
+        uint64_t V = or_mulmod(a[j + t], S, q);
+        a[j] = or_addmod(U, V, q);
+        a[j + t] = or_submod(U, V, q);
+      }
+    }
+  }
+}
+
+/* INTT^{GS,psi^-1}_{bo->no} (Eq. 1): Gentleman-Sande
+ * butterflies, bit-reversed input, natural output, then x N^{-1}. */
+void or_ntt_inv(uint64_t* a, uint32_t logn, uint64_t q, const uint64_t* inv, uint64_t ninv) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t t = 1;
+  for (uint64_t m = n; m > 1; m >>= 1) {
+    uint64_t h = m >> 1, j1 = 0;
+    for (uint64_t i = 0; i < h; ++i) {
+      uint64_t S = inv[h + i];
+      for (uint64_t j = j1; j < j1 + t; ++j) {
+        uint64_t U = a[j];
+        uint64_t V = a[j + t];
+        a[j] = or_addmod(U, V, q);
+        a[j + t] = or_mulmod(or_submod(U, V, q), S, q);
+      }
+      j1 += 2 * t;
+    }
+    t <<= 1;
+  }
+  for (uint64_t j = 0; j < n; ++j) a[j] = or_mulmod(a[j], ninv, q);
+}
+
+/* The (.) of Eq. 1: c_k = a_k * b_k mod q. */
+void or_pointwise(uint64_t* c, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q) {
+  for (uint64_t k = 0; k < n; ++k) c[k] = or_mulmod(a[k], b[k], q);
+}
+
+/* ----------------------------------------------------------- definitions */
+
+/* The plain definition the CT loop computes: output slot k is
+ * the evaluation of a at the root psi^{2 brv(k) + 1} of x^N + 1:
+ *   NTT(a)[k] = sum_i a_i * psi^{(2 brv(k) + 1) i}  mod q.   O(N) per k. */
+uint64_t or_naive_ntt_at(const uint64_t* a, uint32_t logn, uint64_t q, uint64_t psi, uint32_t k) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t zeta = or_powmod(psi, 2 * (uint64_t)or_brv(k, logn) + 1, q);
+  uint64_t acc = 0, pw = 1;
+  for (uint64_t i = 0; i < n; ++i) {
+    acc = or_addmod(acc, or_mulmod(a[i], pw, q), q);
+    pw = or_mulmod(pw, zeta, q);
+  }
+  return acc;
+}
+
+void or_naive_ntt(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, uint64_t psi) {
+  uint64_t n = (uint64_t)1 << logn;
+  for (uint64_t k = 0; k < n; ++k) out[k] = or_naive_ntt_at(a, logn, q, psi, (uint32_t)k);
+}
+
+/* Inverse of the definition above: a_i = N^{-1} sum_k A[k] psi^{-(2 brv(k)+1) i}. */
+uint64_t or_naive_intt_at(const uint64_t* A, uint32_t logn, uint64_t q, uint64_t psi, uint32_t i) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t psi_inv = or_powmod(psi, q - 2, q);
+  uint64_t acc = 0;
+  for (uint64_t k = 0; k < n; ++k) {
+    uint64_t e = ((2 * (uint64_t)or_brv((uint32_t)k, logn) + 1) * (uint64_t)i) % (2 * n);
+    acc = or_addmod(acc, or_mulmod(A[k], or_powmod(psi_inv, e, q), q), q);
+  }
+  return or_mulmod(acc, or_powmod(n % q, q - 2, q), q);
+}
+
+/* Schoolbook negacyclic product:
+ *   c_k = sum_{i+j=k} a_i b_j - sum_{i+j=k+N} a_i b_j  mod q.   O(N) per k. */
+uint64_t or_schoolbook_at(const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q, uint32_t k) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t acc = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (i <= k) {
+      acc = or_addmod(acc, or_mulmod(a[i], b[k - i], q), q);
+    } else {
+      acc = or_submod(acc, or_mulmod(a[i], b[n + k - i], q), q);
+    }
+  }
+  return acc;
+}
+
+void or_schoolbook(uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q) {
+  uint64_t n = (uint64_t)1 << logn;
+  for (uint64_t k = 0; k < n; ++k) c[k] = or_schoolbook_at(a, b, logn, q, (uint32_t)k);
+}
+
+/* ---------------------------------------------------------- batch driver */
+/* Layout (reading C10): [batch][n_limbs][N], limb l uses moduli[l], psi[l].
+ * op: 0 forward, 1 inverse, 2 polymul-with-eval-operand c = INTT(NTT(a) . b_hat),
+ *     3 full polymul c = INTT(NTT(a) . NTT(b)).  b is [b_batch][n_limbs][N]
+ *     with b_batch in {1, batch} (1 = broadcast). */
+
+typedef struct {
+  uint64_t* data;
+  const uint64_t* b;
+  uint32_t batch, n_limbs, logn, b_bcast;
+  const uint64_t* moduli;
+  uint64_t** fwd;
+  uint64_t** inv;
+  const uint64_t* ninv;
+  int op;
+  uint64_t unit_begin, unit_end;
+} or_job;
+
+static void run_unit(const or_job* J, uint64_t u, uint64_t* scratch) {
+  uint64_t n = (uint64_t)1 << J->logn;
+  uint32_t l = (uint32_t)(u % J->n_limbs);
+  uint64_t bidx = u / J->n_limbs;
+  uint64_t q = J->moduli[l];
+  uint64_t* a = J->data + u * n;
+  if (J->op == 0) {
+    or_ntt_fwd(a, J->logn, q, J->fwd[l]);
+  } else if (J->op == 1) {
+    or_ntt_inv(a, J->logn, q, J->inv[l], J->ninv[l]);
+  } else {
+    const uint64_t* b = J->b + ((J->b_bcast ? 0 : bidx) * J->n_limbs + l) * n;
+    or_ntt_fwd(a, J->logn, q, J->fwd[l]);
+    if (J->op == 3) {
+      memcpy(scratch, b, n * sizeof(uint64_t));
+      or_ntt_fwd(scratch, J->logn, q, J->fwd[l]);
+      b = scratch;
+    }
+    or_pointwise(a, a, b, n, q);
+    or_ntt_inv(a, J->logn, q, J->inv[l], J->ninv[l]);
+  }
+}
+
+static void* run_job(void* arg) {
+  const or_job* J = (const or_job*)arg;
+  uint64_t n = (uint64_t)1 << J->logn;
+  uint64_t* scratch = (uint64_t*)malloc(n * sizeof(uint64_t));
+  for (uint64_t u = J->unit_begin; u < J->unit_end; ++u) run_unit(J, u, scratch);
+  free(scratch);
+  return NULL;
+}
+
+int or_batch(int op, uint64_t* data, const uint64_t* b, int b_bcast, uint32_t batch,
+             uint32_t n_limbs, uint32_t logn, const uint64_t* moduli, const uint64_t* psi,
+             int n_threads) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t units = (uint64_t)batch * n_limbs;
+  if (units == 0) return 0;
+  uint64_t** fwd = (uint64_t**)calloc(n_limbs, sizeof(uint64_t*));
+  uint64_t** inv = (uint64_t**)calloc(n_limbs, sizeof(uint64_t*));
+  uint64_t* ninv = (uint64_t*)calloc(n_limbs, sizeof(uint64_t));
+  for (uint32_t l = 0; l < n_limbs; ++l) {
+    fwd[l] = (uint64_t*)malloc(n * sizeof(uint64_t));
+    inv[l] = (uint64_t*)malloc(n * sizeof(uint64_t));
+    or_tables(moduli[l], psi[l], logn, fwd[l], inv[l], &ninv[l]);
+  }
+  if (n_threads < 1) n_threads = 1;
+  if ((uint64_t)n_threads > units) n_threads = (int)units;
+  pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+  or_job* jobs = (or_job*)calloc((size_t)n_threads, sizeof(or_job));
+  for (int t = 0; t < n_threads; ++t) {
+    or_job J = {data, b, batch, n_limbs, logn, (uint32_t)b_bcast, moduli, fwd, inv, ninv, op,
+                units * (uint64_t)t / (uint64_t)n_threads,
+                units * (uint64_t)(t + 1) / (uint64_t)n_threads};
+    jobs[t] = J;
+    pthread_create(&th[t], NULL, run_job, &jobs[t]);
+  }
+  for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+  for (uint32_t l = 0; l < n_limbs; ++l) { free(fwd[l]); free(inv[l]); }
+  free(fwd); free(inv); free(ninv); free(th); free(jobs);
+  return 0;
+}

@@ -1,0 +1,36 @@
+/* ntt_oracle.h -- CPU oracle (TEST INFRASTRUCTURE ONLY; see ntt_oracle.c).
+ * Private to oracle/: the product's include/ never includes this file. */
+#ifndef NTT_ORACLE_H
+#define NTT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+uint64_t or_mulmod(uint64_t a, uint64_t b, uint64_t q);
+uint64_t or_addmod(uint64_t a, uint64_t b, uint64_t q);
+uint64_t or_submod(uint64_t a, uint64_t b, uint64_t q);
+uint64_t or_powmod(uint64_t base, uint64_t e, uint64_t q);
+int or_is_prime(uint64_t n);
+uint32_t or_brv(uint32_t i, uint32_t logn);
+int or_is_primitive_2n_root(uint64_t psi, uint64_t q, uint32_t logn);
+uint64_t or_min_psi(uint64_t q, uint32_t logn);
+int or_primes(uint32_t logn, uint32_t count, uint64_t* out);
+void or_tables(uint64_t q, uint64_t psi, uint32_t logn, uint64_t* fwd, uint64_t* inv, uint64_t* ninv);
+void or_ntt_fwd(uint64_t* a, uint32_t logn, uint64_t q, const uint64_t* fwd);
+void or_ntt_inv(uint64_t* a, uint32_t logn, uint64_t q, const uint64_t* inv, uint64_t ninv);
+void or_pointwise(uint64_t* c, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q);
+uint64_t or_naive_ntt_at(const uint64_t* a, uint32_t logn, uint64_t q, uint64_t psi, uint32_t k);
+void or_naive_ntt(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, uint64_t psi);
+uint64_t or_naive_intt_at(const uint64_t* A, uint32_t logn, uint64_t q, uint64_t psi, uint32_t i);
+uint64_t or_schoolbook_at(const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q, uint32_t k);
+void or_schoolbook(uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q);
+int or_batch(int op, uint64_t* data, const uint64_t* b, int b_bcast, uint32_t batch,
+             uint32_t n_limbs, uint32_t logn, const uint64_t* moduli, const uint64_t* psi,
+             int n_threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
