@@ -1,0 +1,158 @@
+"""B200-native batched negacyclic NTT / INTT / polymul in RNS form.
+
+Thin ctypes binding over librnsntt.so (C ABI: include/rnsntt.h).  Every step
+of the path runs in the library's sm_100a kernels; this module only
+marshals arguments.  There is no CPU fallback: importing the package on a
+box without the built library raises immediately.
+
+Functions keep the C names without the ``rnt_`` prefix:
+
+    plan = Plan(log2n, moduli, psi=None, device=0)
+    ntt_forward(plan, out, inp)             # NTT^{CT,psi}_{no->bo}  (Eq. 1)
+    ntt_inverse(plan, out, inp)             # INTT^{GS,psi^-1}_{bo->no} incl. N^{-1}
+    pointwise_mul(plan, c, a_hat, b_hat)    # the (.) of Eq. 1
+    polymul(plan, c, a, b, b_is_eval=False) # Eq. 1 end to end
+
+Tensors are CUDA tensors of dtype torch.uint64 (or torch.int64 used as raw
+64-bit storage), contiguous, shaped [batch, n_limbs, N] (or any shape with
+batch*n_limbs*N elements; batch is inferred).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _lib
+from ._lib import (RNT_E_CUDA, RNT_E_INVALID_ARG, RNT_E_MODULUS, RNT_E_OOM, RNT_E_PLAN_MISMATCH,
+                   RNT_E_ROOT, RNT_E_UNSUPPORTED_N, RNT_OK, RntError, launch_count, lib_path,
+                   status_string)
+
+__all__ = [
+    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "execute_host",
+    "RntError", "status_string", "launch_count", "lib_path",
+    "RNT_OK", "RNT_E_INVALID_ARG", "RNT_E_UNSUPPORTED_N", "RNT_E_MODULUS", "RNT_E_ROOT",
+    "RNT_E_PLAN_MISMATCH", "RNT_E_CUDA", "RNT_E_OOM",
+    "OP_FORWARD", "OP_INVERSE", "OP_POLYMUL_EVAL", "OP_POLYMUL",
+]
+
+OP_FORWARD, OP_INVERSE, OP_POLYMUL_EVAL, OP_POLYMUL = 0, 1, 2, 3
+
+
+class Plan:
+    """rnt_plan: N = 2^log2n, one ~60-bit NTT-friendly prime per limb."""
+
+    def __init__(self, log2n: int, moduli, psi=None, device: int | None = None):
+        if device is None:
+            import torch
+
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        mods = [int(m) for m in moduli]
+        L = len(mods)
+        marr = (ctypes.c_uint64 * max(L, 1))(*mods)
+        parr = None
+        if psi is not None:
+            ps = [int(x) for x in psi]
+            if len(ps) != L:
+                raise ValueError("psi must have one entry per modulus")
+            parr = (ctypes.c_uint64 * L)(*ps)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.L.rnt_plan_create(ctypes.byref(h), log2n, L, marr, parr, device))
+        self._h = h
+        self.log2n = log2n
+        self.n = 1 << log2n
+        self.n_limbs = L
+        self.moduli = mods
+        self.device = device
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RntError(RNT_E_INVALID_ARG, "plan destroyed")
+        return self._h
+
+    def psi(self):
+        out = (ctypes.c_uint64 * self.n_limbs)()
+        _lib.check(_lib.L.rnt_plan_query(self.handle, None, None, out, None))
+        return [int(v) for v in out]
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.L.rnt_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+def _ptr(t) -> int:
+    if hasattr(t, "data_ptr"):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("expected a contiguous CUDA tensor")
+        return t.data_ptr()
+    return int(t)
+
+
+def _batch(plan: Plan, t, batch):
+    if batch is not None:
+        return int(batch)
+    per = plan.n_limbs * plan.n
+    numel = t.numel()
+    if numel % per:
+        raise ValueError(f"tensor of {numel} elements is not a whole number of [L={plan.n_limbs}][N={plan.n}] polynomials")
+    return numel // per
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def ntt_forward(plan: Plan, out, inp, batch=None, stream=None) -> None:
+    """NTT^{CT,psi}_{no->bo} of every limb of every polynomial (Eq. 1)."""
+    b = _batch(plan, inp, batch)
+    _lib.check(_lib.L.rnt_ntt_forward(plan.handle, _ptr(out), _ptr(inp), b, _stream(stream)))
+
+
+def ntt_inverse(plan: Plan, out, inp, batch=None, stream=None) -> None:
+    """INTT^{GS,psi^-1}_{bo->no} including N^{-1} (Eq. 1)."""
+    b = _batch(plan, inp, batch)
+    _lib.check(_lib.L.rnt_ntt_inverse(plan.handle, _ptr(out), _ptr(inp), b, _stream(stream)))
+
+
+def pointwise_mul(plan: Plan, c, a_hat, b_hat, batch=None, b_broadcast=False, stream=None) -> None:
+    """c = a_hat (.) b_hat mod q_l (NTT domain)."""
+    b = _batch(plan, a_hat, batch)
+    _lib.check(_lib.L.rnt_pointwise_mul(plan.handle, _ptr(c), _ptr(a_hat), _ptr(b_hat), b,
+                                        int(bool(b_broadcast)), _stream(stream)))
+
+
+def polymul(plan: Plan, c, a, b_op, b_is_eval=False, batch=None, b_broadcast=False, stream=None) -> None:
+    """c = a * b mod (x^N + 1) per limb via Eq. 1 (b_op in NTT form if b_is_eval)."""
+    b = _batch(plan, a, batch)
+    _lib.check(_lib.L.rnt_polymul(plan.handle, _ptr(c), _ptr(a), _ptr(b_op), b, int(bool(b_is_eval)),
+                                  int(bool(b_broadcast)), _stream(stream)))
+
+
+def execute_host(plan: Plan, op: int, out_host, in_host, dev_ws, b_dev=None, batch=None,
+                 b_broadcast=False, stream=None) -> None:
+    """Host buffers in/out (pinned recommended): H2D copy, op, D2H copy, async."""
+    hb = _batch(plan, in_host, batch)
+    op_ptr = in_host.data_ptr() if hasattr(in_host, "data_ptr") else int(in_host)
+    out_ptr = out_host.data_ptr() if hasattr(out_host, "data_ptr") else int(out_host)
+    bptr = _ptr(b_dev) if b_dev is not None else None
+    _lib.check(_lib.L.rnt_execute_host(plan.handle, int(op), out_ptr, op_ptr, _ptr(dev_ws), bptr, hb,
+                                       int(bool(b_broadcast)), _stream(stream)))

@@ -1,0 +1,419 @@
+// api.cu -- C ABI (include/rnsntt.h) over the sm_100a kernels.
+//
+// Dispatch (reading C14): N = 2^4 .. 2^10 -> one-kernel team NTT (ntt_small.cuh);
+// N = 2^11 .. 2^16 -> two-pass column/row NTT (ntt_large.cuh).  Every entry
+// point validates its arguments on the host before launching anything and
+// never synchronises the stream.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/rnsntt.h"
+#include "modarith.cuh"
+#include "ntt_large.cuh"
+#include "ntt_small.cuh"
+#include "plan.h"
+
+using namespace rnt;
+
+struct rnt_plan_s {
+  uint32_t logn = 0, L = 0;
+  int device = 0;
+  std::vector<HostLimb> limbs;
+  LimbC* d_lc = nullptr;
+  TW* d_fwd = nullptr;      // team layout (n <= 10) or row layout (n >= 11), [L][N]
+  TW* d_inv = nullptr;
+  TW* d_col_fwd = nullptr;  // n >= 11: natural entries [L][2^{n1}]
+  TW* d_col_inv = nullptr;
+};
+
+static thread_local int g_last_cuda = 0;
+static std::atomic<uint64_t> g_launches{0};
+
+static rnt_status cuda_fail(cudaError_t e) {
+  g_last_cuda = (int)e;
+  return e == cudaErrorMemoryAllocation ? RNT_E_OOM : RNT_E_CUDA;
+}
+
+#define RNT_CUDA(call)                         \
+  do {                                         \
+    cudaError_t e_ = (call);                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_); \
+  } while (0)
+
+static rnt_status after_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RNT_OK : cuda_fail(e);
+}
+
+// ------------------------------------------------------------------ kernels
+// Elementwise (.) of Eq. 1 with canonical output: mont(mont(a, b), R^2) = a b mod q.
+__global__ void k_pointwise(u64* __restrict__ c, const u64* __restrict__ a, const u64* __restrict__ b,
+                            int b_bcast, const LimbC* __restrict__ lc, uint32_t L, uint32_t logn,
+                            uint64_t total2) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total2; v += stride) {
+    const uint64_t e = v * 2;
+    const uint64_t u = e >> logn;
+    const uint32_t l = (uint32_t)(u % L);
+    const uint64_t k = e & ((1ull << logn) - 1);
+    const u64 q = lc[l].q, qinv = lc[l].qinv, r2 = lc[l].r2;
+    const ulonglong2 av = __ldg(reinterpret_cast<const ulonglong2*>(a) + v);
+    const uint64_t bi = b_bcast ? (((uint64_t)l << logn) + k) : e;
+    const ulonglong2 bv = __ldg(reinterpret_cast<const ulonglong2*>(b + bi));
+    ulonglong2 cv;
+    cv.x = canon2(mont_mul(mont_mul(av.x, bv.x, q, qinv), r2, q, qinv), q);
+    cv.y = canon2(mont_mul(mont_mul(av.y, bv.y, q, qinv), r2, q, qinv), q);
+    reinterpret_cast<ulonglong2*>(c)[v] = cv;
+  }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, d);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// ---------------------------------------------------------------- launchers
+template <int LOGN, int MODE>
+static rnt_status launch_team(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
+                              int bcast, uint64_t units, cudaStream_t st) {
+  static bool attr_set = false;  // benign race: idempotent attribute call
+  const size_t smem = team_smem_bytes<LOGN, MODE>();
+  if (!attr_set) {
+    RNT_CUDA(cudaFuncSetAttribute(k_team<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const uint64_t per_cta = (uint64_t)kTeamWarps * TeamCfg<LOGN>::TEAMS;
+  const uint64_t grid = (units + per_cta - 1) / per_cta;
+  k_team<LOGN, MODE><<<(unsigned)grid, kTeamWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv,
+                                                                   p->d_lc, p->L, units);
+  return after_launch();
+}
+
+template <int MODE>
+static rnt_status team_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                uint64_t units, cudaStream_t st) {
+  switch (p->logn) {
+    case 4: return launch_team<4, MODE>(p, out, in, bop, bcast, units, st);
+    case 5: return launch_team<5, MODE>(p, out, in, bop, bcast, units, st);
+    case 6: return launch_team<6, MODE>(p, out, in, bop, bcast, units, st);
+    case 7: return launch_team<7, MODE>(p, out, in, bop, bcast, units, st);
+    case 8: return launch_team<8, MODE>(p, out, in, bop, bcast, units, st);
+    case 9: return launch_team<9, MODE>(p, out, in, bop, bcast, units, st);
+    case 10: return launch_team<10, MODE>(p, out, in, bop, bcast, units, st);
+    default: return RNT_E_UNSUPPORTED_N;
+  }
+}
+
+// CTA order for the two-pass kernels: block b -> (sub-block, poly, limb) with
+// the sub-block fastest, then the polynomial, then the limb, so CTAs that
+// share a limb's twiddle rows run back to back (L2 reuse across the batch).
+template <int LOGN>
+static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
+                             uint32_t batch, cudaStream_t st) {
+  using P = TwoPass<LOGN>;
+  const uint64_t units = (uint64_t)batch * p->L;
+  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
+    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
+    dim3 g(P::Cn / kColTile, (unsigned)cnt);
+    if (inv)
+      k_col_inv<LOGN><<<g, P::P1_THREADS, 0, st>>>(out, in, p->d_col_inv, p->d_lc, p->L, batch, y0, after_mont);
+    else
+      k_col_fwd<LOGN><<<g, P::P1_THREADS, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
+}
+
+template <int LOGN, int MODE>
+static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                             uint32_t batch, cudaStream_t st) {
+  using P = TwoPass<LOGN>;
+  const uint64_t units = (uint64_t)batch * p->L;
+  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
+    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
+    dim3 g(P::R / P::RPC, (unsigned)cnt);
+    k_row<LOGN, MODE><<<g, P::P2_THREADS, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv, p->d_lc, p->L,
+                                                  batch, y0);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
+}
+
+template <int LOGN>
+static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                           uint32_t batch, cudaStream_t st) {
+  rnt_status s;
+  switch (op) {
+    case 0:  // forward
+      if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
+      return launch_row<LOGN, 0>(p, out, out, nullptr, 0, batch, st);
+    case 1:  // inverse
+      if ((s = launch_row<LOGN, 1>(p, out, in, nullptr, 0, batch, st)) != RNT_OK) return s;
+      return launch_col<LOGN>(p, true, 0, out, out, batch, st);
+    case 2:  // c = INTT(NTT(a) . b_hat)
+      if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
+      if ((s = launch_row<LOGN, 2>(p, out, out, bop, bcast, batch, st)) != RNT_OK) return s;
+      return launch_col<LOGN>(p, true, 1, out, out, batch, st);
+    default: return RNT_E_INVALID_ARG;
+  }
+}
+
+static rnt_status large_dispatch(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop,
+                                 int bcast, uint32_t batch, cudaStream_t st) {
+  switch (p->logn) {
+    case 11: return large_op<11>(p, op, out, in, bop, bcast, batch, st);
+    case 12: return large_op<12>(p, op, out, in, bop, bcast, batch, st);
+    case 13: return large_op<13>(p, op, out, in, bop, bcast, batch, st);
+    case 14: return large_op<14>(p, op, out, in, bop, bcast, batch, st);
+    case 15: return large_op<15>(p, op, out, in, bop, bcast, batch, st);
+    case 16: return large_op<16>(p, op, out, in, bop, bcast, batch, st);
+    default: return RNT_E_UNSUPPORTED_N;
+  }
+}
+
+// ------------------------------------------------------------------- checks
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static rnt_status check_plan_device(const rnt_plan_s* p) {
+  int d = -1;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return d == p->device ? RNT_OK : RNT_E_PLAN_MISMATCH;
+}
+
+static rnt_status check_data(const rnt_plan_s* p, const void* a, const void* b, uint32_t batch) {
+  if (!p) return RNT_E_INVALID_ARG;
+  if (batch == 0) return RNT_OK;
+  if (!a || !b || !aligned16(a) || !aligned16(b)) return RNT_E_INVALID_ARG;
+  const unsigned __int128 bytes = (unsigned __int128)batch * p->L * (1ull << p->logn) * 8u;
+  if (bytes >> 62) return RNT_E_INVALID_ARG;
+  return check_plan_device(p);
+}
+
+// --------------------------------------------------------------------- ABI
+extern "C" {
+
+const char* rnt_status_string(rnt_status s) {
+  switch (s) {
+    case RNT_OK: return "RNT_OK";
+    case RNT_E_INVALID_ARG: return "RNT_E_INVALID_ARG: invalid argument";
+    case RNT_E_UNSUPPORTED_N: return "RNT_E_UNSUPPORTED_N: log2n outside [4, 16]";
+    case RNT_E_MODULUS: return "RNT_E_MODULUS: modulus not prime, not 1 mod 2N, >= 2^62, or duplicated";
+    case RNT_E_ROOT: return "RNT_E_ROOT: psi is not a primitive 2N-th root of unity";
+    case RNT_E_PLAN_MISMATCH: return "RNT_E_PLAN_MISMATCH: current device differs from the plan's";
+    case RNT_E_CUDA: return "RNT_E_CUDA: CUDA runtime error";
+    case RNT_E_OOM: return "RNT_E_OOM: out of memory";
+  }
+  return "unknown rnt_status";
+}
+
+int rnt_last_cuda_error(void) { return g_last_cuda; }
+
+uint64_t rnt_launch_count(void) { return g_launches.load(); }
+
+rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, const uint64_t* moduli,
+                           const uint64_t* psi, int device) {
+  if (!out || !moduli || n_limbs == 0 || n_limbs > RNT_MAX_LIMBS) return RNT_E_INVALID_ARG;
+  *out = nullptr;
+  if (log2n < RNT_MIN_LOG2N || log2n > RNT_MAX_LOG2N) return RNT_E_UNSUPPORTED_N;
+  std::vector<HostLimb> limbs;
+  int pe = plan_limbs(log2n, n_limbs, moduli, psi, limbs);
+  if (pe == PLAN_E_MODULUS) return RNT_E_MODULUS;
+  if (pe == PLAN_E_ROOT) return RNT_E_ROOT;
+  if (pe != PLAN_OK) return RNT_E_INVALID_ARG;
+
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess) return cuda_fail(ce);
+  if (device < 0 || device >= ndev) return RNT_E_INVALID_ARG;
+  int prev = 0;
+  RNT_CUDA(cudaGetDevice(&prev));
+  RNT_CUDA(cudaSetDevice(device));
+
+  rnt_plan_s* p = new (std::nothrow) rnt_plan_s;
+  if (!p) return RNT_E_OOM;
+  p->logn = log2n;
+  p->L = n_limbs;
+  p->device = device;
+  p->limbs = limbs;
+  const uint32_t n = 1u << log2n;
+  const uint32_t n1 = (log2n + 1) / 2;
+  const bool large = log2n > 10;
+
+  std::vector<LimbC> lc(n_limbs);
+  for (uint32_t l = 0; l < n_limbs; ++l) {
+    const HostLimb& h = limbs[l];
+    lc[l].q = h.q;
+    lc[l].q2 = h.q2;
+    lc[l].qinv = h.qinv;
+    lc[l].r2 = h.r2;
+    lc[l].ninv = TW{h.ninv.w, h.ninv.wp};
+    lc[l].ninv_w1 = TW{h.ninv_w1.w, h.ninv_w1.wp};
+    lc[l].ninvR = TW{h.ninvR.w, h.ninvR.wp};
+    lc[l].ninvR_w1 = TW{h.ninvR_w1.w, h.ninvR_w1.wp};
+  }
+  std::vector<HostTW> nat(n), lay((size_t)n_limbs * n), layi((size_t)n_limbs * n);
+  std::vector<HostTW> col, coli;
+  if (large) {
+    col.resize((size_t)n_limbs << n1);
+    coli.resize((size_t)n_limbs << n1);
+  }
+  for (uint32_t l = 0; l < n_limbs; ++l) {
+    for (int dir = 0; dir < 2; ++dir) {
+      plan_powers(limbs[l], log2n, dir == 1, n, nat.data());
+      HostTW* dst = (dir ? layi.data() : lay.data()) + (size_t)l * n;
+      if (large) {
+        plan_row_layout(nat.data(), log2n, dst);
+        std::memcpy((dir ? coli.data() : col.data()) + ((size_t)l << n1), nat.data(), sizeof(HostTW) << n1);
+      } else {
+        plan_team_layout(nat.data(), log2n, dst);
+      }
+    }
+  }
+  auto fail = [&](cudaError_t e) {
+    rnt_plan_destroy(p);
+    cudaSetDevice(prev);
+    return cuda_fail(e);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->d_lc, sizeof(LimbC) * n_limbs)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&p->d_fwd, sizeof(TW) * lay.size())) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&p->d_inv, sizeof(TW) * layi.size())) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(p->d_lc, lc.data(), sizeof(LimbC) * n_limbs, cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(p->d_fwd, lay.data(), sizeof(TW) * lay.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(p->d_inv, layi.data(), sizeof(TW) * layi.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  if (large) {
+    if ((e = cudaMalloc(&p->d_col_fwd, sizeof(TW) * col.size())) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&p->d_col_inv, sizeof(TW) * coli.size())) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpy(p->d_col_fwd, col.data(), sizeof(TW) * col.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpy(p->d_col_inv, coli.data(), sizeof(TW) * coli.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  }
+  cudaSetDevice(prev);
+  *out = p;
+  return RNT_OK;
+}
+
+rnt_status rnt_plan_destroy(rnt_plan p) {
+  if (!p) return RNT_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaFree(p->d_lc);
+  cudaFree(p->d_fwd);
+  cudaFree(p->d_inv);
+  cudaFree(p->d_col_fwd);
+  cudaFree(p->d_col_inv);
+  cudaSetDevice(prev);
+  delete p;
+  return RNT_OK;
+}
+
+rnt_status rnt_plan_query(rnt_plan p, uint32_t* log2n, uint32_t* n_limbs, uint64_t* psi_out, int* device) {
+  if (!p) return RNT_E_INVALID_ARG;
+  if (log2n) *log2n = p->logn;
+  if (n_limbs) *n_limbs = p->L;
+  if (device) *device = p->device;
+  if (psi_out)
+    for (uint32_t l = 0; l < p->L; ++l) psi_out[l] = p->limbs[l].psi;
+  return RNT_OK;
+}
+
+static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_, const uint64_t* b_, int bcast,
+                         uint32_t batch, cudaStream_t st) {
+  u64* out = reinterpret_cast<u64*>(out_);
+  const u64* in = reinterpret_cast<const u64*>(in_);
+  const u64* b = reinterpret_cast<const u64*>(b_);
+  const uint64_t units = (uint64_t)batch * p->L;
+  if (p->logn <= 10) {
+    switch (op) {
+      case 0: return team_dispatch<0>(p, out, in, nullptr, 0, units, st);
+      case 1: return team_dispatch<1>(p, out, in, nullptr, 0, units, st);
+      case 2: return team_dispatch<2>(p, out, in, b, bcast, units, st);
+      case 3: return team_dispatch<3>(p, out, in, b, bcast, units, st);
+    }
+    return RNT_E_INVALID_ARG;
+  }
+  if (op == 3) {
+    // NTT(b) into a stream-ordered temporary, then the fused eval-form path.
+    const uint64_t bunits = bcast ? p->L : units;
+    const size_t bytes = (size_t)bunits << (p->logn + 3);
+    u64* tmp = nullptr;
+    RNT_CUDA(cudaMallocAsync(&tmp, bytes, st));
+    rnt_status s = large_dispatch(p, 0, tmp, b, nullptr, 0, bcast ? 1u : batch, st);
+    if (s == RNT_OK) s = large_dispatch(p, 2, out, in, tmp, bcast, batch, st);
+    cudaError_t e = cudaFreeAsync(tmp, st);
+    if (s == RNT_OK && e != cudaSuccess) return cuda_fail(e);
+    return s;
+  }
+  return large_dispatch(p, op, out, in, b, bcast, batch, st);
+}
+
+rnt_status rnt_ntt_forward(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {
+  rnt_status s = check_data(p, out, in, batch);
+  if (s != RNT_OK || batch == 0) return s;
+  return run_op(p, 0, out, in, nullptr, 0, batch, (cudaStream_t)stream);
+}
+
+rnt_status rnt_ntt_inverse(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {
+  rnt_status s = check_data(p, out, in, batch);
+  if (s != RNT_OK || batch == 0) return s;
+  return run_op(p, 1, out, in, nullptr, 0, batch, (cudaStream_t)stream);
+}
+
+rnt_status rnt_pointwise_mul(rnt_plan p, uint64_t* c, const uint64_t* a_hat, const uint64_t* b_hat, uint32_t batch,
+                             int b_broadcast, void* stream) {
+  rnt_status s = check_data(p, c, a_hat, batch);
+  if (s != RNT_OK || batch == 0) return s;
+  if (!b_hat || !aligned16(b_hat)) return RNT_E_INVALID_ARG;
+  const uint64_t total2 = ((uint64_t)batch * p->L << p->logn) / 2;
+  const int threads = 256;
+  uint64_t blocks = (total2 + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  k_pointwise<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<u64*>(c), reinterpret_cast<const u64*>(a_hat), reinterpret_cast<const u64*>(b_hat), b_broadcast ? 1 : 0, p->d_lc,
+                                                                      p->L, p->logn, total2);
+  return after_launch();
+}
+
+rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t batch, int b_is_eval,
+                       int b_broadcast, void* stream) {
+  rnt_status s = check_data(p, c, a, batch);
+  if (s != RNT_OK || batch == 0) return s;
+  if (!b || !aligned16(b) || b == c) return RNT_E_INVALID_ARG;
+  return run_op(p, b_is_eval ? 2 : 3, c, a, b, b_broadcast ? 1 : 0, batch, (cudaStream_t)stream);
+}
+
+rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uint64_t* in_host, uint64_t* dev_ws,
+                            const uint64_t* b_dev, uint32_t batch, int b_broadcast, void* stream) {
+  if (!p || (int)op < 0 || (int)op > 3) return RNT_E_INVALID_ARG;
+  if (batch == 0) return RNT_OK;
+  if (!out_host || !in_host) return RNT_E_INVALID_ARG;
+  rnt_status s = check_data(p, dev_ws, dev_ws, batch);
+  if (s != RNT_OK) return s;
+  if ((op == RNT_OP_POLYMUL_EVAL || op == RNT_OP_POLYMUL) && (!b_dev || !aligned16(b_dev) || b_dev == dev_ws))
+    return RNT_E_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = ((size_t)batch * p->L << p->logn) * 8;
+  RNT_CUDA(cudaMemcpyAsync(dev_ws, in_host, bytes, cudaMemcpyHostToDevice, st));
+  s = run_op(p, (int)op, dev_ws, dev_ws, b_dev, b_broadcast ? 1 : 0, batch, st);
+  if (s != RNT_OK) return s;
+  RNT_CUDA(cudaMemcpyAsync(out_host, dev_ws, bytes, cudaMemcpyDeviceToHost, st));
+  return RNT_OK;
+}
+
+}  // extern "C"

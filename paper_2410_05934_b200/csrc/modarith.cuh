@@ -1,0 +1,106 @@
+// modarith.cuh -- 64-bit modular arithmetic for sm_100a built from 32-bit
+// IMAD / IMAD.HI / IMAD.WIDE (no tensor cores; BASELINE.json north_star (b)).
+//
+// Moduli: q < 2^62 (reading C5), so lazy ranges up to [0, 4q) fit in a word.
+//
+//   shoup_lazy(y, W)   y * w mod q for any y < 2^64, result in [0, 2q);
+//                      W = (w, w' = floor(w 2^64 / q)) precomputed (Shoup).
+//   ct_bfly            Cooley-Tukey butterfly of NTT^{CT,psi}_{no->bo}
+//                      (Eq. 1): (X, Y) -> (X + wY, X - wY), Harvey's
+//                      lazy form: inputs and outputs in [0, 4q).
+//   gs_bfly            Gentleman-Sande butterfly of INTT^{GS,psi^-1}_{bo->no}
+//                      (Eq. 1): (X, Y) -> (X + Y, (X - Y) w), lazy:
+//                      inputs and outputs in [0, 2q).
+//   mont_mul           a b 2^{-64} mod q (Montgomery), a < 4q, b < q,
+//                      result in (0, 2q); used for the (.) of Eq. 1.
+#pragma once
+#include <stdint.h>
+
+#include <type_traits>
+
+namespace rnt {
+
+typedef unsigned long long u64;
+
+// Compile-time loop: f(std::integral_constant<int, i>) for i in [B, E).  The
+// stage loops below nest loops whose trip counts depend on the stage index;
+// forcing them through templates guarantees full unrolling, so the
+// coefficient arrays stay in registers (no local-memory stack frame).
+template <int B, int E, typename F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    sfor<B + 1, E>(f);
+  }
+}
+
+struct __align__(16) TW {
+  u64 w;   // twiddle value, canonical
+  u64 wp;  // Shoup companion floor(w * 2^64 / q)
+};
+
+// Per-limb constants, device resident.
+struct __align__(16) LimbC {
+  u64 q, q2;     // q, 2q
+  u64 qinv;      // q^{-1} mod 2^64 (Montgomery)
+  u64 r2;        // 2^128 mod q (Montgomery R^2)
+  TW ninv;       // N^{-1}
+  TW ninv_w1;    // N^{-1} * psi^{-brv(1)}: last GS stage with N^{-1} folded
+  TW ninvR;      // N^{-1} * 2^64: after a Montgomery pointwise product
+  TW ninvR_w1;   // N^{-1} * 2^64 * psi^{-brv(1)}
+};
+
+__device__ __forceinline__ u64 ldg_u64(const u64* p) { return __ldg(p); }
+
+__device__ __forceinline__ TW ldg_tw(const TW* p) {
+  ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  TW t;
+  t.w = v.x;
+  t.wp = v.y;
+  return t;
+}
+
+__device__ __forceinline__ u64 shoup_lazy(u64 y, TW t, u64 q) {
+  u64 Q = __umul64hi(y, t.wp);
+  return y * t.w - Q * q;
+}
+
+__device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  u64 x = csub(X, q2);          // [0, 2q)
+  u64 v = shoup_lazy(Y, t, q);  // [0, 2q)
+  X = x + v;                    // [0, 4q)
+  Y = x + q2 - v;               // (0, 4q)
+}
+
+__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  u64 s = csub(X + Y, q2);      // [0, 2q)
+  u64 d = X + q2 - Y;           // (0, 4q)
+  X = s;
+  Y = shoup_lazy(d, t, q);      // [0, 2q)
+}
+
+// Last GS stage (t = N/2, twiddle psi^{-brv(1)}) with the N^{-1} scaling of
+// S:167 folded in: X' = (X + Y) N^{-1}, Y' = (X - Y) psi^{-brv(1)} N^{-1}.
+__device__ __forceinline__ void gs_bfly_last(u64& X, u64& Y, TW s0, TW s1, u64 q, u64 q2) {
+  u64 s = X + Y;                // [0, 4q)
+  u64 d = X + q2 - Y;           // (0, 4q)
+  X = shoup_lazy(s, s0, q);     // [0, 2q)
+  Y = shoup_lazy(d, s1, q);
+}
+
+// [0, 4q) -> [0, q)
+__device__ __forceinline__ u64 canon4(u64 x, u64 q, u64 q2) { return csub(csub(x, q2), q); }
+// [0, 2q) -> [0, q)
+__device__ __forceinline__ u64 canon2(u64 x, u64 q) { return csub(x, q); }
+
+__device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 q, u64 qinv) {
+  u64 lo = a * b;
+  u64 hi = __umul64hi(a, b);
+  u64 m = lo * qinv;            // m q == lo (mod 2^64)
+  u64 mh = __umul64hi(m, q);
+  return hi - mh + q;           // (a b - m q) / 2^64 + q in (0, 2q)
+}
+
+}  // namespace rnt

@@ -1,0 +1,303 @@
+// ntt_large.cuh -- two-pass negacyclic NTT / INTT / fused polymul for
+// N = 2^11 .. 2^16 (the CKKS polynomial size), batched over
+// (polynomial, limb) units (RNS limbs).
+//
+// View a limb as a 2^{n1} x 2^{n2} row-major matrix M[r][c] = a[r 2^{n2} + c]
+// (n1 = ceil(n/2) column stages, n2 = floor(n/2) row stages; 256 x 256 at 2^16).
+// CT stage s pairs j with j + N/2^{s+1} and uses twiddle w[2^s + (j >> (n-s))]:
+//   * stages 0 .. n1-1 only mix elements of one column c and their twiddle
+//     depends only on the row r        -> pass 1 ("columns"),
+//   * stages n1 .. n-1 only mix elements of one row r      -> pass 2 ("rows").
+// This is the B200 analogue of the paper's coefficient shuffling + switching
+// point (prior art): exactly one global exchange (the kernel
+// boundary; the 22.5 MiB cfg3 intermediate stays L2-resident, 126 MB L2),
+// and every other exchange is a shared-memory transpose inside one CTA
+// (pass 1: one __syncthreads) or one half-warp (pass 2: __syncwarp only).
+//
+// Inside a pass every thread holds E = 16 coefficients in registers:
+//   sub-pass A: the 4 stages with distance >= 16 threads (stride layout),
+//   sub-pass B: the remaining <= 4 stages (16 contiguous coefficients).
+// Global loads/stores are always in the stride layout, i.e. coalesced
+// 16 x 8 B = 128 B per half-warp row segment.
+#pragma once
+#include "modarith.cuh"
+#include "ntt_small.cuh"   // cp_async8
+
+namespace rnt {
+
+constexpr int kEl = 16;       // coefficients per thread
+constexpr int kColTile = 16;  // columns per pass-1 CTA (one 128-byte line per row)
+
+template <int LOGN>
+struct TwoPass {
+  static constexpr int n = LOGN;
+  static constexpr int n1 = (LOGN + 1) / 2;   // column stages
+  static constexpr int n2 = LOGN / 2;         // row stages
+  static constexpr int R = 1 << n1;           // rows
+  static constexpr int Cn = 1 << n2;          // columns (row length)
+  static constexpr int T1 = R / kEl;          // threads per column
+  static constexpr int T2 = Cn / kEl;         // threads per row
+  static constexpr int P1_THREADS = kColTile * T1;
+  static constexpr int RPC = (256 / T2) < R ? (256 / T2) : R;  // rows per pass-2 CTA
+  static constexpr int P2_THREADS = RPC * T2;                   // <= 256
+  static constexpr int ROWBUF = Cn + T2;      // padded row buffer (elements)
+  static_assert(n1 >= 4 && n1 <= 8 && n2 >= 5 && n2 <= 8, "two-pass covers 2^10..2^16");
+};
+
+// Swizzle inside a row buffer: conflict-free for c = c0 + T2*i and c = 16*c1 + i'.
+template <int LOGN>
+__device__ __forceinline__ int row_swz(int c) {
+  return c ^ ((c >> 4) & (TwoPass<LOGN>::T2 - 1));
+}
+
+// ============================== pass 1 (columns) ==============================
+// Forward: CT stages 0..n1-1 on columns [cb*16, cb*16+16) of unit u.
+// MODE 0: plain forward (in -> out).
+template <int LOGN>
+__global__ void __launch_bounds__(TwoPass<LOGN>::P1_THREADS)
+k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
+          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+  using P = TwoPass<LOGN>;
+  __shared__ __align__(16) u64 tile[P::R * kColTile];
+  const int c = threadIdx.x % kColTile;
+  const int r0 = threadIdx.x / kColTile;
+  const uint64_t y = y0 + blockIdx.y;          // y = limb * B + poly (limb-major CTA order)
+  const uint32_t l = (uint32_t)(y / B);
+  const uint64_t u = (y % B) * L + l;
+  const u64 q = lc[l].q, q2 = lc[l].q2;
+  const TW* T = tw_col + (size_t)l * P::R;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * kColTile + c;
+  u64 x[kEl];
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(r0 + P::T1 * i) * P::Cn];
+  // sub-pass A: stages 0..3, twiddle w[2^s + (i >> (4-s))] (uniform)
+  sfor<0, 4>([&](auto S_) {
+    constexpr int s = decltype(S_)::value;
+    constexpr int half = kEl >> (s + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << s); ++blk) {
+      TW w = ldg_tw(T + (1 << s) + blk);
+#pragma unroll
+      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+    }
+  });
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) tile[(r0 + P::T1 * i) * kColTile + c] = x[i];
+  __syncthreads();
+  const int r1 = r0;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = tile[(kEl * r1 + i) * kColTile + c];
+  // sub-pass B: stages 4..n1-1 on rows 16 r1 + i; twiddle w[2^s + ((16 r1 + i) >> (n1 - s))]
+  sfor<4, P::n1>([&](auto S_) {
+    constexpr int s = decltype(S_)::value;
+    constexpr int t = P::R >> (s + 1);
+#pragma unroll
+    for (int m = 0; m < kEl / (2 * t); ++m) {
+      TW w = ldg_tw(T + (1 << s) + ((kEl * r1 + m * 2 * t) >> (P::n1 - s)));
+#pragma unroll
+      for (int k = 0; k < t; ++k) ct_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+    }
+  });
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) out[base + (size_t)(kEl * r1 + i) * P::Cn] = x[i];
+}
+
+// Inverse: GS stages n1-1..0 (+ N^{-1} or N^{-1} R scaling), canonical output.
+template <int LOGN>
+__global__ void __launch_bounds__(TwoPass<LOGN>::P1_THREADS)
+k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
+          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
+  using P = TwoPass<LOGN>;
+  __shared__ __align__(16) u64 tile[P::R * kColTile];
+  const int c = threadIdx.x % kColTile;
+  const int r1 = threadIdx.x / kColTile;
+  const uint64_t y = y0 + blockIdx.y;
+  const uint32_t l = (uint32_t)(y / B);
+  const uint64_t u = (y % B) * L + l;
+  const u64 q = lc[l].q, q2 = lc[l].q2;
+  const TW* T = tw_col + (size_t)l * P::R;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * kColTile + c;
+  u64 x[kEl];
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(kEl * r1 + i) * P::Cn];
+  sfor<0, P::n1 - 4>([&](auto I_) {
+    constexpr int s = P::n1 - 1 - decltype(I_)::value;
+    constexpr int t = P::R >> (s + 1);
+#pragma unroll
+    for (int m = 0; m < kEl / (2 * t); ++m) {
+      TW w = ldg_tw(T + (1 << s) + ((kEl * r1 + m * 2 * t) >> (P::n1 - s)));
+#pragma unroll
+      for (int k = 0; k < t; ++k) gs_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+    }
+  });
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) tile[(kEl * r1 + i) * kColTile + c] = x[i];
+  __syncthreads();
+  const int r0 = r1;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = tile[(r0 + P::T1 * i) * kColTile + c];
+  sfor<0, 3>([&](auto I_) {
+    constexpr int s = 3 - decltype(I_)::value;
+    constexpr int half = kEl >> (s + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << s); ++blk) {
+      TW w = ldg_tw(T + (1 << s) + blk);
+#pragma unroll
+      for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+    }
+  });
+  const TW s0 = after_mont ? lc[l].ninvR : lc[l].ninv;
+  const TW s1 = after_mont ? lc[l].ninvR_w1 : lc[l].ninv_w1;
+#pragma unroll
+  for (int k = 0; k < kEl / 2; ++k) gs_bfly_last(x[k], x[k + kEl / 2], s0, s1, q, q2);
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) out[base + (size_t)(r0 + P::T1 * i) * P::Cn] = canon2(x[i], q);
+}
+
+// ============================== pass 2 (rows) =================================
+// Row twiddle table (per limb, per row r, 2^{n2} entries): stage v (global
+// stage n1 + v) occupies [2^v - 1, 2^{v+1} - 1); for v < 4 entry k holds
+// w[2^{n1+v} + r 2^v + k]; for v >= 4 entry m*T2 + c1 holds
+// w[2^{n1+v} + r 2^v + c1 2^{v+4-n2} + m] (lane-major: coalesced loads).
+
+template <int LOGN>
+__device__ __forceinline__ void row_fwd_A(u64 (&x)[kEl], const TW* Tr, u64 q, u64 q2) {
+  sfor<0, 4>([&](auto V_) {
+    constexpr int v = decltype(V_)::value;
+    constexpr int half = kEl >> (v + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << v); ++blk) {
+      TW w = ldg_tw(Tr + (1 << v) - 1 + blk);
+#pragma unroll
+      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+    }
+  });
+}
+
+template <int LOGN>
+__device__ __forceinline__ void row_fwd_B(u64 (&x)[kEl], const TW* Tr, int c1, u64 q, u64 q2) {
+  using P = TwoPass<LOGN>;
+  sfor<4, P::n2>([&](auto V_) {
+    constexpr int v = decltype(V_)::value;
+    constexpr int t = P::Cn >> (v + 1);
+#pragma unroll
+    for (int m = 0; m < kEl / (2 * t); ++m) {
+      TW w = ldg_tw(Tr + (1 << v) - 1 + m * P::T2 + c1);
+#pragma unroll
+      for (int k = 0; k < t; ++k) ct_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+    }
+  });
+}
+
+template <int LOGN>
+__device__ __forceinline__ void row_inv_B(u64 (&x)[kEl], const TW* Tr, int c1, u64 q, u64 q2) {
+  using P = TwoPass<LOGN>;
+  sfor<0, P::n2 - 4>([&](auto I_) {
+    constexpr int v = P::n2 - 1 - decltype(I_)::value;
+    constexpr int t = P::Cn >> (v + 1);
+#pragma unroll
+    for (int m = 0; m < kEl / (2 * t); ++m) {
+      TW w = ldg_tw(Tr + (1 << v) - 1 + m * P::T2 + c1);
+#pragma unroll
+      for (int k = 0; k < t; ++k) gs_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+    }
+  });
+}
+
+template <int LOGN>
+__device__ __forceinline__ void row_inv_A(u64 (&x)[kEl], const TW* Tr, u64 q, u64 q2) {
+  sfor<0, 4>([&](auto I_) {
+    constexpr int v = 3 - decltype(I_)::value;
+    constexpr int half = kEl >> (v + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << v); ++blk) {
+      TW w = ldg_tw(Tr + (1 << v) - 1 + blk);
+#pragma unroll
+      for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+    }
+  });
+}
+
+// stride layout (c = c0 + T2 i) -> contiguous layout (c = 16 c1 + i)
+template <int LOGN>
+__device__ __forceinline__ void row_A_to_B(u64 (&x)[kEl], u64* rb, int c0) {
+  using P = TwoPass<LOGN>;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) rb[row_swz<LOGN>(c0 + P::T2 * i)] = x[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = rb[row_swz<LOGN>(kEl * c0 + i)];
+  __syncwarp();
+}
+
+template <int LOGN>
+__device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
+  using P = TwoPass<LOGN>;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) rb[row_swz<LOGN>(kEl * c0 + i)] = x[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = rb[row_swz<LOGN>(c0 + P::T2 * i)];
+  __syncwarp();
+}
+
+// MODE 0: forward rows (CT stages n1..n-1, canonical output)
+// MODE 1: inverse rows (GS stages n-1..n1, lazy [0,2q) output for k_col_inv)
+// MODE 2: fused forward rows -> (.) b_hat (Montgomery) -> inverse rows
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(TwoPass<LOGN>::P2_THREADS)
+k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
+      const TW* __restrict__ tw_row_fwd, const TW* __restrict__ tw_row_inv,
+      const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+  using P = TwoPass<LOGN>;
+  __shared__ __align__(16) u64 sbuf[P::RPC * P::ROWBUF];
+  const int c0 = threadIdx.x % P::T2;
+  const int rr = threadIdx.x / P::T2;
+  const int r = blockIdx.x * P::RPC + rr;
+  const uint64_t y = y0 + blockIdx.y;
+  const uint32_t l = (uint32_t)(y / B);
+  const uint64_t u = (y % B) * L + l;
+  const u64 q = lc[l].q, q2 = lc[l].q2;
+  u64* rb = sbuf + rr * P::ROWBUF;
+  const size_t rowoff = u * (size_t)(P::R * P::Cn) + (size_t)r * P::Cn;
+  const size_t troff = ((size_t)l * P::R + r) * P::Cn;
+  u64 x[kEl];
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) x[i] = in[rowoff + c0 + P::T2 * i];
+  if (MODE == 1) {
+    row_A_to_B<LOGN>(x, rb, c0);
+    row_inv_B<LOGN>(x, tw_row_inv + troff, c0, q, q2);
+    row_B_to_A<LOGN>(x, rb, c0);
+    row_inv_A<LOGN>(x, tw_row_inv + troff, q, q2);
+  } else {
+    const TW* Tf = tw_row_fwd + troff;
+    row_fwd_A<LOGN>(x, Tf, q, q2);
+    row_A_to_B<LOGN>(x, rb, c0);
+    if (MODE == 2) {
+      const u64* bsrc = bop + (b_bcast ? (size_t)l * P::R * P::Cn : u * (size_t)(P::R * P::Cn)) + (size_t)r * P::Cn;
+#pragma unroll
+      for (int i = 0; i < kEl; ++i) cp_async8(rb + row_swz<LOGN>(c0 + P::T2 * i), bsrc + c0 + P::T2 * i);
+    }
+    row_fwd_B<LOGN>(x, Tf, c0, q, q2);
+    if (MODE == 0) {
+#pragma unroll
+      for (int i = 0; i < kEl; ++i) x[i] = canon4(x[i], q, q2);
+      row_B_to_A<LOGN>(x, rb, c0);
+    } else {
+      cp_async_wait_all();
+      __syncwarp();
+      const u64 qinv = lc[l].qinv;
+#pragma unroll
+      for (int i = 0; i < kEl; ++i) x[i] = mont_mul(x[i], rb[row_swz<LOGN>(kEl * c0 + i)], q, qinv);
+      __syncwarp();
+      const TW* Ti = tw_row_inv + troff;
+      row_inv_B<LOGN>(x, Ti, c0, q, q2);
+      row_B_to_A<LOGN>(x, rb, c0);
+      row_inv_A<LOGN>(x, Ti, q, q2);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) out[rowoff + c0 + P::T2 * i] = x[i];
+}
+
+}  // namespace rnt

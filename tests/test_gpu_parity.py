@@ -1,0 +1,280 @@
+"""GPU parity: the sm_100a kernels through the C ABI versus the CPU oracle,
+bit-exact on every element (integer work, BASELINE.json north_star).
+
+Inputs come from inputs/ (SplitMix64 + Lemire, seeded); expected values come
+only from oracle/.  P:n = PAPER.md line n.
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle as O
+from helpers import empty_dev, from_dev, params, to_dev
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2410_05934_b200 as R  # noqa: E402
+
+ALL_LOGN = list(range(4, 17))
+
+
+def _plan(logn, limbs):
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    assert p.psi() == list(psi)  # plan's reading-C1 psi equals the oracle's
+    return p, ps, psi
+
+
+def _batch_for(logn):
+    return {4: 37, 5: 33, 6: 19, 7: 9, 8: 9, 9: 5, 10: 7}.get(logn, 2)
+
+
+@pytest.mark.parametrize("logn", ALL_LOGN)
+def test_forward_inverse_all_sizes(logn):
+    limbs = 3
+    B = _batch_for(logn)
+    p, ps, psi = _plan(logn, limbs)
+    n = 1 << logn
+    a = inputs.residues(100 + logn, B, ps, n)
+    want = O.batch(O.OP_FWD, a, ps, psi, n_threads=8)
+    da = to_dev(a)
+    dout = empty_dev(a.shape)
+    R.ntt_forward(p, dout, da)
+    got = from_dev(dout)
+    assert np.array_equal(got, want)
+    # inverse of the oracle's forward output must give back a
+    dback = empty_dev(a.shape)
+    R.ntt_inverse(p, dback, to_dev(want))
+    assert np.array_equal(from_dev(dback), a)
+    # inverse on random eval-domain input vs the oracle inverse
+    A = inputs.residues(200 + logn, B, ps, n)
+    R.ntt_inverse(p, dback, to_dev(A))
+    assert np.array_equal(from_dev(dback), O.batch(O.OP_INV, A, ps, psi, n_threads=8))
+
+
+@pytest.mark.parametrize("logn", ALL_LOGN)
+@pytest.mark.parametrize("bcast", [False, True])
+def test_polymul_all_sizes(logn, bcast):
+    limbs = 2
+    B = _batch_for(logn)
+    p, ps, psi = _plan(logn, limbs)
+    n = 1 << logn
+    a = inputs.residues(300 + logn, B, ps, n)
+    b = inputs.residues(400 + logn, 1 if bcast else B, ps, n)
+    want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, b_broadcast=bcast, n_threads=8)
+    bhat = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+    dc = empty_dev(a.shape)
+    R.polymul(p, dc, to_dev(a), to_dev(b), b_is_eval=False, b_broadcast=bcast)
+    assert np.array_equal(from_dev(dc), want)
+    R.polymul(p, dc, to_dev(a), to_dev(bhat), b_is_eval=True, b_broadcast=bcast)
+    assert np.array_equal(from_dev(dc), want)
+    # sampled schoolbook on the GPU result itself
+    got = from_dev(dc)
+    for k in (0, n // 3, n - 1):
+        assert int(got[0, 0, k]) == O.schoolbook_at(a[0, 0], b[0, 0], ps[0], k)
+
+
+@pytest.mark.parametrize("logn", [4, 10, 12, 16])
+def test_pointwise(logn):
+    p, ps, psi = _plan(logn, 3)
+    n = 1 << logn
+    B = 3
+    a = inputs.residues(5, B, ps, n)
+    b = inputs.residues(6, B, ps, n)
+    dc = empty_dev(a.shape)
+    R.pointwise_mul(p, dc, to_dev(a), to_dev(b))
+    want = np.stack([np.stack([O.pointwise(a[i, l], b[i, l], ps[l]) for l in range(3)]) for i in range(B)])
+    assert np.array_equal(from_dev(dc), want)
+    R.pointwise_mul(p, dc, to_dev(a), to_dev(b[:1]), b_broadcast=True)
+    want = np.stack([np.stack([O.pointwise(a[i, l], b[0, l], ps[l]) for l in range(3)]) for i in range(B)])
+    assert np.array_equal(from_dev(dc), want)
+
+
+@pytest.mark.parametrize("logn", [4, 7, 10, 11, 16])
+def test_edge_inputs(logn):
+    """zeros, all q-1 (max lazy range), delta_0, delta_{N-1}, alternating, monomials."""
+    n = 1 << logn
+    p, ps, psi = _plan(logn, 2)
+    rows = []
+    for l, q in enumerate(ps):
+        pass
+    vecs = []
+    z = np.zeros((2, n), dtype=np.uint64)
+    vecs.append(z.copy())
+    vecs.append(np.array([[q - 1] * n for q in ps], dtype=np.uint64))
+    d0 = z.copy(); d0[:, 0] = 1; vecs.append(d0)
+    dl = z.copy(); dl[:, -1] = 1; vecs.append(dl)
+    alt = np.array([[0 if i % 2 == 0 else q - 1 for i in range(n)] for q in ps], dtype=np.uint64)
+    vecs.append(alt)
+    for j in (1, n // 2, n - 2):
+        m = z.copy(); m[:, j] = 1; vecs.append(m)
+    a = np.stack(vecs)  # [B][L][N]
+    want = O.batch(O.OP_FWD, a, ps, psi)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    got = from_dev(d)
+    assert np.array_equal(got, want)
+    assert np.all(got[2] == 1)  # NTT(delta_0) = 1
+    R.ntt_inverse(p, d, to_dev(np.ones_like(a)))
+    back = from_dev(d)
+    assert np.all(back[:, :, 0] == 1) and np.all(back[:, :, 1:] == 0)
+    # polymul of extremes: (q-1 ... ) * (q-1 ...)
+    c = empty_dev(a.shape)
+    R.polymul(p, c, to_dev(a), to_dev(a[::-1].copy()))
+    assert np.array_equal(from_dev(c), O.batch(O.OP_POLYMUL, a, ps, psi, b=a[::-1].copy()))
+
+
+@pytest.mark.parametrize("logn", [6, 10, 13, 16])
+def test_in_place(logn):
+    p, ps, psi = _plan(logn, 2)
+    a = inputs.residues(8, 3, ps, 1 << logn)
+    d = to_dev(a)
+    R.ntt_forward(p, d, d)
+    assert np.array_equal(from_dev(d), O.batch(O.OP_FWD, a, ps, psi))
+    R.ntt_inverse(p, d, d)
+    assert np.array_equal(from_dev(d), a)
+    b = inputs.residues(9, 3, ps, 1 << logn)
+    R.polymul(p, d, d, to_dev(b))
+    assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL, a, ps, psi, b=b))
+
+
+def test_tiny_prime_spec_example():
+    """q = 97, N = 16 on the GPU: NTT(0..15) worked value and S:171 convolution."""
+    p = R.Plan(4, [97])
+    assert p.psi() == [19]
+    a = np.arange(16, dtype=np.uint64).reshape(1, 1, 16)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    assert list(map(int, from_dev(d).ravel())) == [13, 72, 27, 49, 55, 96, 18, 8, 60, 8, 32, 51, 36, 67, 67, 20]
+    rng = np.random.default_rng(0)
+    A = rng.integers(0, 97, (50, 1, 16)).astype(np.uint64)
+    Bm = rng.integers(0, 97, (50, 1, 16)).astype(np.uint64)
+    R.polymul(p, empty_dev(A.shape), to_dev(A), to_dev(Bm))
+    c = empty_dev(A.shape)
+    R.polymul(p, c, to_dev(A), to_dev(Bm))
+    got = from_dev(c)
+    for i in range(50):
+        assert np.array_equal(got[i, 0], O.schoolbook(A[i, 0], Bm[i, 0], 97))
+
+
+def test_explicit_psi():
+    logn = 10
+    ps, _ = params(logn, 1)
+    q = ps[0]
+    psi_min = O.min_psi(q, logn)
+    other = pow(psi_min, 3, q)  # also a primitive 2N-th root (odd power)
+    p = R.Plan(logn, [q], psi=[other])
+    a = inputs.residues(1, 2, [q], 1 << logn)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    assert np.array_equal(from_dev(d), O.batch(O.OP_FWD, a, [q], [other]))
+
+
+def test_roundtrip_100_trials():
+    # SPEC S:164 / acceptance #1: 100 trials per N in {2^10, 2^12, 2^13, 2^16}
+    for logn in (10, 12, 13, 16):
+        p, ps, psi = _plan(logn, 1)
+        a = inputs.residues(77, 100, ps, 1 << logn)
+        d = to_dev(a)
+        R.ntt_forward(p, d, d)
+        R.ntt_inverse(p, d, d)
+        assert np.array_equal(from_dev(d), a)
+
+
+def test_cfg1_seeded_digest_matches_survey():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "survey_appendix_a.json")))
+    q = g["q10"]
+    p = R.Plan(10, [q])
+    a = inputs.residues(0, 1, [q], 1024)
+    b = inputs.residues(1, 1, [q], 1024)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    assert inputs.digest(from_dev(d)) == (g["cfg1_seed0"]["ntt_sum"], g["cfg1_seed0"]["ntt_wsum"])
+    R.polymul(p, d, to_dev(a), to_dev(b))
+    assert inputs.digest(from_dev(d)) == (g["cfg1_seed0"]["polymul_sum"], g["cfg1_seed0"]["polymul_wsum"])
+
+
+# ------------------------------------------------------------- full configs
+def test_cfg2_full_bitexact():
+    """TFHE batch: N=2^10, 4096 polys: NTT -> (.) b_hat -> INTT, every element."""
+    ps, psi = params(10, 1)
+    p = R.Plan(10, ps)
+    a = inputs.residues(0, 4096, ps, 1024)
+    b = inputs.residues(1, 4096, ps, 1024)
+    bhat = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    assert np.array_equal(from_dev(d), O.batch(O.OP_FWD, a, ps, psi, n_threads=8))
+    R.polymul(p, d, to_dev(a), to_dev(bhat), b_is_eval=True)
+    assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bhat, n_threads=8))
+
+
+def test_cfg3_full_bitexact():
+    """CKKS HMUL-sized: N=2^16, 45 limbs, NTT -> (.) b_hat -> INTT (reading C8)."""
+    ps, psi = params(16, 45)
+    p = R.Plan(16, ps)
+    a = inputs.residues(0, 1, ps, 1 << 16)
+    b = inputs.residues(1, 1, ps, 1 << 16)
+    bhat = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+    d = empty_dev(a.shape)
+    R.polymul(p, d, to_dev(a), to_dev(bhat), b_is_eval=True)
+    got = from_dev(d)
+    assert np.array_equal(got, O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bhat, n_threads=8))
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "survey_appendix_a.json")))["cfg3_seed0"]
+    assert inputs.digest(got[0, 0]) == (g["limb0"]["polymul_sum"], g["limb0"]["polymul_wsum"])
+    assert inputs.digest(got[0, 44]) == (g["limb44"]["polymul_sum"], g["limb44"]["polymul_wsum"])
+
+
+def test_cfg4_full_bitexact():
+    """N=2^16, 60 limbs x 8 polys, forward + inverse, every element."""
+    ps, psi = params(16, 60)
+    p = R.Plan(16, ps)
+    a = inputs.residues(0, 8, ps, 1 << 16)
+    d = to_dev(a)
+    R.ntt_forward(p, d, d)
+    fwd = from_dev(d)
+    assert np.array_equal(fwd, O.batch(O.OP_FWD, a, ps, psi, n_threads=8))
+    R.ntt_inverse(p, d, d)
+    assert np.array_equal(from_dev(d), a)
+
+
+def test_streams_and_concurrency():
+    ps, psi = params(16, 4)
+    p = R.Plan(16, ps)
+    a = inputs.residues(3, 2, ps, 1 << 16)
+    want = O.batch(O.OP_FWD, a, ps, psi)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    d1, d2 = to_dev(a), to_dev(a)
+    torch.cuda.synchronize()
+    R.ntt_forward(p, d1, d1, stream=s1)
+    R.ntt_forward(p, d2, d2, stream=s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(d1), want) and np.array_equal(from_dev(d2), want)
+
+
+def test_execute_host_roundtrip():
+    ps, psi = params(10, 1)
+    p = R.Plan(10, ps)
+    a = inputs.residues(4, 64, ps, 1024)
+    hin = torch.from_numpy(a.view(np.int64).copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    ws = empty_dev(a.shape)
+    R.execute_host(p, R.OP_FORWARD, hout, hin, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy().view(np.uint64), O.batch(O.OP_FWD, a, ps, psi))
+
+
+def test_batch_zero_is_noop_and_errors():
+    ps, _ = params(10, 1)
+    p = R.Plan(10, ps)
+    d = empty_dev((1, 1, 1024))
+    R.ntt_forward(p, d, d, batch=0)
+    with pytest.raises(R.RntError) as e:
+        R.ntt_forward(p, d.view(-1)[1:], d, batch=1)  # misaligned pointer
+    assert e.value.code == R.RNT_E_INVALID_ARG
