@@ -1,0 +1,415 @@
+"""Benchmark: batched negacyclic NTT -> (.) -> INTT on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5]
+                    [--impl ours|reference] [--scaling weak|strong]
+
+One *step* is one pass of the whole hot path
+over one batch of synthetic input: for every (polynomial, limb) unit,
+c = INTT(NTT(a) (.) b_hat) (Eq. 1; reading C8: b_hat is an
+NTT-form operand resident on the device, like an evaluation key or an RGSW
+row).  The default workload is BASELINE.json configs[4] (cfg5), the config
+the metric names both halves of: N=2^16 x 45 limbs (CKKS) plus N=2^10 x 16384
+polynomials (TFHE).  `value` counts limb-transforms (one forward or one
+inverse N-point transform of one limb) per second over all ranks.
+
+Multi-GPU (torchrun): weak scaling by default -- rank r owns polynomial
+batch index r of the global problem (inputs generated from the global
+counters, so shards are slices of one global array); no collective touches
+the data path.  Timing: per-step CUDA events on the launching stream with an
+L2 flush (256 MiB write) between steps outside the events, W warm-up steps,
+barrier + synchronize around the timed region, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import inputs  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "limb-transforms/s"
+
+# Workloads (BASELINE.json configs).  parts: (log2n, limbs, polys, seed)
+WORKLOADS = {
+    "cfg1": {"desc": "N=2^10, one 60-bit prime, single polynomial, NTT -> (.) b_hat -> INTT",
+             "parts": [(10, 1, 1, 0)]},
+    "cfg2": {"desc": "N=2^10, one 60-bit prime, 4096 polynomials, NTT -> (.) b_hat -> INTT",
+             "parts": [(10, 1, 4096, 0)]},
+    "cfg3": {"desc": "N=2^16, 45 limbs, one polynomial, NTT -> (.) b_hat -> INTT",
+             "parts": [(16, 45, 1, 0)]},
+    "cfg4": {"desc": "N=2^16, 60 limbs x 8 polynomials, NTT -> (.) b_hat -> INTT",
+             "parts": [(16, 60, 8, 0)]},
+    "cfg5": {"desc": "N=2^16 x 45 limbs + N=2^10 x 16384 polynomials, NTT -> (.) b_hat -> INTT",
+             "parts": [(16, 45, 1, 0), (10, 1, 16384, 0)]},
+}
+
+L2_FLUSH_BYTES = 256 << 20
+FMA_SLOTS_PER_BFLY = 16   # exact Shoup butterfly: 6 wide/hi multiplies x 2 + 4 IMAD
+IMAD_SLOTS_PER_CLK_SM = 64
+N_SM = 148
+
+
+def primes_for(logn: int, limbs: int):
+    # Workload parameter, reading C2: the `limbs` largest primes q < 2^60 with
+    # q = 1 mod 2N (the library validates them again in rnt_plan_create).
+    two_n = 2 << logn
+    out = []
+    k = ((1 << 60) - 1) // two_n
+    while len(out) < limbs:
+        q = k * two_n + 1
+        if _is_prime(q):
+            out.append(q)
+        k -= 1
+    return out
+
+
+def _is_prime(n: int) -> bool:
+    if n < 2:
+        return False
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if n % p == 0:
+            return n == p
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.05):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self.period = period
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        busy = [s for s in self.samples if s > 0]
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": sorted(self.reasons - {"gpu_idle"})}
+
+
+# --------------------------------------------------------------- reference
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def make_part_inputs(logn, limbs, polys, seed, poly_offset):
+    mods = primes_for(logn, limbs)
+    a = inputs.residues(seed, polys, mods, 1 << logn, batch_offset=poly_offset)
+    bhat = inputs.residues(seed + 1, polys, mods, 1 << logn, batch_offset=poly_offset)
+    return mods, a, bhat
+
+
+def transforms_per_step(parts) -> int:
+    return sum(2 * limbs * polys for (_, limbs, polys, _) in parts)
+
+
+def bfly_per_step(parts) -> int:
+    return sum(2 * limbs * polys * (1 << logn) // 2 * logn for (logn, limbs, polys, _) in parts)
+
+
+def run_oracle_sample(parts, poly_offset: int, cores: int, min_seconds: float):
+    """Time the CPU oracle (as it stands) on the workload; repeat until min_seconds."""
+    import oracle as O
+
+    data = []
+    for (logn, limbs, polys, seed) in parts:
+        mods, a, bhat = make_part_inputs(logn, limbs, polys, seed, poly_offset)
+        psi = [O.min_psi(q, logn) for q in mods]
+        data.append((mods, psi, a, bhat))
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        for mods, psi, a, bhat in data:
+            O.batch(O.OP_POLYMUL_EVAL, a, mods, psi, b=bhat, n_threads=cores)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    return reps, el
+
+
+def cpu_baseline_block(wl, parts, cores, min_seconds=8.0):
+    reps, el = run_oracle_sample(parts, 0, cores, min_seconds)
+    per = transforms_per_step(parts)
+    return {"value": per * reps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"full {wl} workload x {reps} repetition(s) ({per} limb-transforms each, "
+                      f"{el:.1f} s wall on {cores} threads; oracle = plain C, exact 128-bit %)"}
+
+
+def bench_reference(args, wl, parts):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = cpu_cores()
+    per = transforms_per_step(parts)
+    for _ in range(args.warmup):
+        run_oracle_sample(parts, 0, cores, 0.0)
+    times = []
+    for _ in range(args.steps):
+        reps, el = run_oracle_sample(parts, 0, cores, 0.0)
+        times.append(el)
+    tot = sum(times)
+    value = per * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded SplitMix64 uniform residues)",
+        "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}", "executor": "CPU oracle, all host cores"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"full {wl} workload per step on {cores} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+def bench_ours(args, wl, parts):
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    # ---- shard: weak scaling -> rank r owns global polynomial block r.
+    states = []
+    for (logn, limbs, polys, seed) in parts:
+        off = rank * polys if args.scaling == "weak" else 0
+        mods, a, bhat = make_part_inputs(logn, limbs, polys, seed, off)
+        plan = R.Plan(logn, mods, device=local)
+        da = torch.from_numpy(a.view(np.int64)).to(dev)
+        db = torch.from_numpy(bhat.view(np.int64)).to(dev)
+        dc = torch.empty_like(da)
+        ha = torch.from_numpy(a.view(np.int64)).pin_memory()
+        hc = torch.empty_like(ha).pin_memory()
+        ws_buf = torch.empty_like(da)
+        states.append(dict(logn=logn, limbs=limbs, polys=polys, plan=plan, a=da, b=db, c=dc,
+                           ha=ha, hc=hc, ws=ws_buf))
+    # the dominant kernel: largest butterfly count part
+    work = [(2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]) for s in states]
+    dom = int(np.argmax(work))
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        for i, s in enumerate(states):
+            if ev is not None:
+                ev[i][0].record(stream)
+            R.polymul(s["plan"], s["c"], s["a"], s["b"], b_is_eval=True, stream=stream)
+            if ev is not None:
+                ev[i][1].record(stream)
+
+    def step_host():
+        for s in states:
+            R.execute_host(s["plan"], R.OP_POLYMUL_EVAL, s["hc"], s["ha"], s["ws"], b_dev=s["b"],
+                           stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- device-resident timed region
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in states] for _ in range(args.steps)]
+    launches0 = R.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(args.steps):
+            flush.zero_()   # L2 flush outside the timed events
+            step(evs[k])
+        barrier()
+    launches = R.launch_count() - launches0
+    part_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps)] for i in range(len(states))]
+    step_ms = [sum(part_ms[i][k] for i in range(len(states))) for k in range(args.steps)]
+    total_ms = sum(step_ms)
+
+    # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
+    for _ in range(max(1, args.warmup // 2)):
+        step_host()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for k in range(args.steps):
+        step_host()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = sum(s["a"].numel() * 8 for s in states)
+
+    # ---- max over ranks
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+
+    per_rank = transforms_per_step(parts)
+    value = per_rank * ws * args.steps / (total_ms * 1e-3)
+    e2e_value = per_rank * ws * args.steps / (e2e_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel(s)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9   # Gbfly/s
+    s = states[dom]
+    bfly_launch = 2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]
+    dom_ms = statistics.mean(part_ms[dom])
+    achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{wl}:part{dom}")
+        except Exception:
+            traffic = None
+    kern = "k_team<10,2> (fused NTT->(.)->INTT, N=2^10)" if s["logn"] <= 10 else \
+        "k_col_fwd + k_row<16,2> + k_col_inv (N=2^16 polymul)"
+    roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak_bfly,
+            "unit": "Gbutterfly/s", "frac": achieved / peak_bfly, "traffic": traffic,
+            "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
+                          f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
+    parts_out = []
+    for i, st in enumerate(states):
+        ms = statistics.mean(part_ms[i])
+        xf = 2 * st["limbs"] * st["polys"]
+        bf = xf * (1 << st["logn"]) // 2 * st["logn"]
+        alg_bytes = 3 * st["limbs"] * st["polys"] * (1 << st["logn"]) * 8  # read a, b_hat; write c
+        parts_out.append({"log2n": st["logn"], "limbs": st["limbs"], "polys": st["polys"], "ms": ms,
+                          "limb_transforms_per_s": xf / (ms * 1e-3),
+                          "us_per_limb_transform": ms * 1e3 / xf,
+                          "gbfly_per_s": bf / (ms * 1e-3) / 1e9, "frac_alu": bf / (ms * 1e-3) / 1e9 / peak_bfly,
+                          "alg_hbm_gbs": alg_bytes / (ms * 1e-3) / 1e9})
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded SplitMix64 uniform residues mod 60-bit NTT primes)",
+            "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}",
+                       "l2": "flushed (256 MiB write) between steps, outside the timed events",
+                       "global_polys_per_part": [p[2] * (ws if args.scaling == 'weak' else 1) for p in parts],
+                       "parallelism": f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws}, no data-path collective"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "parts": parts_out,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+            "clocks": clk.summary(),
+        }
+        if args.cpu_baseline and ws >= 1 and rank == 0 and (ws == 1):
+            line["cpu_baseline"] = cpu_baseline_block(wl, parts, cpu_cores())
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak"])
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = args.workload
+    parts = WORKLOADS[wl]["parts"]
+    if args.impl == "reference":
+        bench_reference(args, wl, parts)
+    else:
+        bench_ours(args, wl, parts)
+
+
+if __name__ == "__main__":
+    main()

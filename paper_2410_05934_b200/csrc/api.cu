@@ -1,6 +1,6 @@
 // api.cu -- C ABI (include/rnsntt.h) over the sm_100a kernels.
 //
-// Dispatch (reading C14): N = 2^4 .. 2^10 -> one-kernel team NTT (ntt_small.cuh);
+// Dispatch (reading C14): N = 2^4 .. 2^10 -> one-kernel warp NTT (ntt_small.cuh);
 // N = 2^11 .. 2^16 -> two-pass column/row NTT (ntt_large.cuh).  Every entry
 // point validates its arguments on the host before launching anything and
 // never synchronises the stream.
@@ -25,7 +25,7 @@ struct rnt_plan_s {
   int device = 0;
   std::vector<HostLimb> limbs;
   LimbC* d_lc = nullptr;
-  TW* d_fwd = nullptr;      // team layout (n <= 10) or row layout (n >= 11), [L][N]
+  TW* d_fwd = nullptr;      // natural order (n <= 10) or row layout (n >= 11), [L][N]
   TW* d_inv = nullptr;
   TW* d_col_fwd = nullptr;  // n >= 11: natural entries [L][2^{n1}]
   TW* d_col_inv = nullptr;
@@ -86,32 +86,41 @@ static int num_sms() {
 
 // ---------------------------------------------------------------- launchers
 template <int LOGN, int MODE>
-static rnt_status launch_team(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
-                              int bcast, uint64_t units, cudaStream_t st) {
+static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
+                              int bcast, uint32_t batch, cudaStream_t st) {
   static bool attr_set = false;  // benign race: idempotent attribute call
-  const size_t smem = team_smem_bytes<LOGN, MODE>();
+  const size_t smem = warp_smem_bytes<LOGN, MODE>();
   if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_team<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  const uint64_t per_cta = (uint64_t)kTeamWarps * TeamCfg<LOGN>::TEAMS;
-  const uint64_t grid = (units + per_cta - 1) / per_cta;
-  k_team<LOGN, MODE><<<(unsigned)grid, kTeamWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv,
-                                                                   p->d_lc, p->L, units);
-  return after_launch();
+  const uint64_t per_cta = (uint64_t)kTeamWarps * WarpCfg<LOGN>::P;
+  const uint64_t gx = (batch + per_cta - 1) / per_cta;
+  for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
+    const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
+    dim3 grid((unsigned)gx, nl);
+    // limb offset l0: shift every per-limb base pointer
+    k_warp<LOGN, MODE><<<grid, kTeamWarps * 32, smem, st>>>(out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN),
+                                                           bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
+                                                           p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN),
+                                                           p->d_lc + l0, p->L, batch);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
 }
 
 template <int MODE>
-static rnt_status team_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
-                                uint64_t units, cudaStream_t st) {
+static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                uint32_t batch, cudaStream_t st) {
   switch (p->logn) {
-    case 4: return launch_team<4, MODE>(p, out, in, bop, bcast, units, st);
-    case 5: return launch_team<5, MODE>(p, out, in, bop, bcast, units, st);
-    case 6: return launch_team<6, MODE>(p, out, in, bop, bcast, units, st);
-    case 7: return launch_team<7, MODE>(p, out, in, bop, bcast, units, st);
-    case 8: return launch_team<8, MODE>(p, out, in, bop, bcast, units, st);
-    case 9: return launch_team<9, MODE>(p, out, in, bop, bcast, units, st);
-    case 10: return launch_team<10, MODE>(p, out, in, bop, bcast, units, st);
+    case 4: return launch_warp<4, MODE>(p, out, in, bop, bcast, batch, st);
+    case 5: return launch_warp<5, MODE>(p, out, in, bop, bcast, batch, st);
+    case 6: return launch_warp<6, MODE>(p, out, in, bop, bcast, batch, st);
+    case 7: return launch_warp<7, MODE>(p, out, in, bop, bcast, batch, st);
+    case 8: return launch_warp<8, MODE>(p, out, in, bop, bcast, batch, st);
+    case 9: return launch_warp<9, MODE>(p, out, in, bop, bcast, batch, st);
+    case 10: return launch_warp<10, MODE>(p, out, in, bop, bcast, batch, st);
     default: return RNT_E_UNSUPPORTED_N;
   }
 }
@@ -280,7 +289,7 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
         plan_row_layout(nat.data(), log2n, dst);
         std::memcpy((dir ? coli.data() : col.data()) + ((size_t)l << n1), nat.data(), sizeof(HostTW) << n1);
       } else {
-        plan_team_layout(nat.data(), log2n, dst);
+        std::memcpy(dst, nat.data(), sizeof(HostTW) * n);  // natural order (ntt_small.cuh)
       }
     }
   }
@@ -340,10 +349,10 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   const uint64_t units = (uint64_t)batch * p->L;
   if (p->logn <= 10) {
     switch (op) {
-      case 0: return team_dispatch<0>(p, out, in, nullptr, 0, units, st);
-      case 1: return team_dispatch<1>(p, out, in, nullptr, 0, units, st);
-      case 2: return team_dispatch<2>(p, out, in, b, bcast, units, st);
-      case 3: return team_dispatch<3>(p, out, in, b, bcast, units, st);
+      case 0: return warp_dispatch<0>(p, out, in, nullptr, 0, batch, st);
+      case 1: return warp_dispatch<1>(p, out, in, nullptr, 0, batch, st);
+      case 2: return warp_dispatch<2>(p, out, in, b, bcast, batch, st);
+      case 3: return warp_dispatch<3>(p, out, in, b, bcast, batch, st);
     }
     return RNT_E_INVALID_ARG;
   }

@@ -2,137 +2,43 @@
 // N = 2^4 .. 2^10 (the TFHE polynomial size), batched over
 // (polynomial, limb) units (CMux-level batching).
 //
-// Decomposition (B200 design, replaces the paper's BD/TA/PCS kernels,
-// P:425-498, as prior art): a *team* of S = 2^G lanes owns one
-// polynomial, each lane holding E = 2^e = N/S coefficients in registers
-// (G = floor(n/2), e = n - G; N=1024: 32 lanes x 32 coefficients, one warp).
-//   pass 1: lane l holds coefficients j = l + S*i (i < E).  The first e CT
-//           stages (distance t >= S) pair i with i + t/S inside the lane;
-//           their twiddles depend only on i (warp-uniform loads).
-//   transpose through a swizzled per-team shared-memory buffer (__syncwarp
-//           only, no CTA barrier).
-//   pass 2: lane l holds j = E*l + i.  The last G stages (t < S <= E) are
-//           lane-local again; twiddles come from a lane-major table layout so
-//           each load is one coalesced 16-byte-per-lane access.
-// So the whole transform has one intra-warp exchange (the paper's
-// "synchronisations", drop to one __syncwarp pair) and all global
-// traffic is coalesced.  Lazy Harvey ranges (modarith.cuh); outputs are
-// canonicalised in the last stage.
+// B200 design (the paper's BD/TA/PCS kernels, are prior art):
+//   * one warp owns a 1024-coefficient shared-memory buffer holding 1024/N
+//     polynomials; no CTA-wide barrier anywhere, only __syncwarp;
+//   * the log2 N stages are grouped into passes of <= 4 stages (N = 2^10:
+//     4 + 4 + 2).  In a pass every lane loads radix-2^k groups of
+//     coefficients into registers, runs k CT (or GS) stages, stores back;
+//   * pass bodies are *looped* (not unrolled) over groups, so the whole
+//     kernel is a few kB of SASS and stays resident in the instruction cache
+//     (a fully unrolled 32-coefficient-per-lane design measured 2.3 stall
+//     cycles per instruction waiting on instruction fetch, profiles/);
+//   * the first forward pass reads global memory directly (coalesced, stride
+//     layout) and the last pass of each direction writes global memory;
+//   * polymul fuses last-forward-pass -> (.) b_hat -> first-inverse-pass in
+//     registers (the NTT-domain product never touches shared memory);
+//   * shared-memory index swizzle j ^ ((j >> 4) & 15) makes all three pass
+//     patterns of N = 2^10 conflict-free.
+// Lazy Harvey ranges (modarith.cuh); outputs are canonical.
 #pragma once
 #include "modarith.cuh"
 
 namespace rnt {
 
-template <int LOGN>
-struct TeamCfg {
-  static constexpr int N = 1 << LOGN;
-  static constexpr int G = LOGN / 2;
-  static constexpr int S = 1 << G;        // lanes per team
-  static constexpr int e = LOGN - G;
-  static constexpr int E = 1 << e;        // coefficients per lane
-  static constexpr int TEAMS = 32 / S;    // teams per warp
-};
-
+constexpr int kWarpElems = 1024;          // coefficients per warp buffer
 constexpr int kTeamWarps = 4;             // warps per CTA
 
-// Swizzle of a team buffer index: conflict-free for both j = l + S*i (pass 1)
-// and j = E*l + i (pass 2) access patterns.
 template <int LOGN>
-__device__ __forceinline__ int team_swz(int j) {
-  using C = TeamCfg<LOGN>;
-  return j ^ ((j >> C::e) & (C::E - 1));
-}
+struct WarpCfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int P = kWarpElems / N;             // polynomials per warp
+  static constexpr int K0 = LOGN < 4 ? LOGN : 4;       // stages per pass
+  static constexpr int K1 = (LOGN - K0) < 4 ? (LOGN - K0) : 4;
+  static constexpr int K2 = LOGN - K0 - K1;
+  static constexpr int NPASS = 1 + (K1 > 0) + (K2 > 0);
+  static_assert(K2 <= 4, "N <= 2^12");
+};
 
-// ---- forward stages ------------------------------------------------------
-// Pass 1: CT stages s = 0 .. e-1 on x[i] = a[l + S*i]; twiddle w[2^s + (i >> (e-s))].
-template <int LOGN>
-__device__ __forceinline__ void team_fwd_pass1(u64 (&x)[TeamCfg<LOGN>::E], const TW* T, u64 q, u64 q2) {
-  using C = TeamCfg<LOGN>;
-  sfor<0, C::e>([&](auto S_) {
-    constexpr int s = decltype(S_)::value;
-    constexpr int half = C::E >> (s + 1);
-#pragma unroll
-    for (int blk = 0; blk < (1 << s); ++blk) {
-      TW w = ldg_tw(T + (1 << s) + blk);
-#pragma unroll
-      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
-    }
-  });
-}
-
-// Pass 2: CT stages s = e .. n-1 on x[i] = a[E*l + i]; twiddle of sub-block m
-// is at lane-major position 2^s + m*S + l of the team table.
-template <int LOGN>
-__device__ __forceinline__ void team_fwd_pass2(u64 (&x)[TeamCfg<LOGN>::E], const TW* T, int lane, u64 q, u64 q2) {
-  using C = TeamCfg<LOGN>;
-  sfor<C::e, LOGN>([&](auto S_) {
-    constexpr int s = decltype(S_)::value;
-    constexpr int t = C::N >> (s + 1);
-#pragma unroll
-    for (int m = 0; m < (1 << (s - C::G)); ++m) {
-      TW w = ldg_tw(T + (1 << s) + m * C::S + lane);
-#pragma unroll
-      for (int k = 0; k < t; ++k) ct_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
-    }
-  });
-}
-
-// ---- inverse stages (mirror) ---------------------------------------------
-template <int LOGN>
-__device__ __forceinline__ void team_inv_pass2(u64 (&x)[TeamCfg<LOGN>::E], const TW* T, int lane, u64 q, u64 q2) {
-  using C = TeamCfg<LOGN>;
-  sfor<0, LOGN - C::e>([&](auto I_) {
-    constexpr int s = LOGN - 1 - decltype(I_)::value;
-    constexpr int t = C::N >> (s + 1);
-#pragma unroll
-    for (int m = 0; m < (1 << (s - C::G)); ++m) {
-      TW w = ldg_tw(T + (1 << s) + m * C::S + lane);
-#pragma unroll
-      for (int k = 0; k < t; ++k) gs_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
-    }
-  });
-}
-
-// GS stages s = e-1 .. 1, then stage 0 with N^{-1} (times s0/s1) folded in.
-template <int LOGN>
-__device__ __forceinline__ void team_inv_pass1(u64 (&x)[TeamCfg<LOGN>::E], const TW* T, TW s0, TW s1, u64 q, u64 q2) {
-  using C = TeamCfg<LOGN>;
-  sfor<0, C::e - 1>([&](auto I_) {
-    constexpr int s = C::e - 1 - decltype(I_)::value;
-    constexpr int half = C::E >> (s + 1);
-#pragma unroll
-    for (int blk = 0; blk < (1 << s); ++blk) {
-      TW w = ldg_tw(T + (1 << s) + blk);
-#pragma unroll
-      for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
-    }
-  });
-#pragma unroll
-  for (int k = 0; k < C::E / 2; ++k) gs_bfly_last(x[k], x[k + C::E / 2], s0, s1, q, q2);
-}
-
-// ---- shared-memory transposes -----------------------------------------------
-template <int LOGN>
-__device__ __forceinline__ void team_p1_to_p2(u64 (&x)[TeamCfg<LOGN>::E], u64* buf, int lane) {
-  using C = TeamCfg<LOGN>;
-#pragma unroll
-  for (int i = 0; i < C::E; ++i) buf[team_swz<LOGN>(lane + C::S * i)] = x[i];
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < C::E; ++i) x[i] = buf[team_swz<LOGN>(C::E * lane + i)];
-  __syncwarp();
-}
-
-template <int LOGN>
-__device__ __forceinline__ void team_p2_to_p1(u64 (&x)[TeamCfg<LOGN>::E], u64* buf, int lane) {
-  using C = TeamCfg<LOGN>;
-#pragma unroll
-  for (int i = 0; i < C::E; ++i) buf[team_swz<LOGN>(C::E * lane + i)] = x[i];
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < C::E; ++i) x[i] = buf[team_swz<LOGN>(lane + C::S * i)];
-  __syncwarp();
-}
+__device__ __forceinline__ int wswz(int j) { return j ^ ((j >> 4) & 15); }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -140,99 +46,291 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// ---- kernels ------------------------------------------------------------------
-// Work unit u = polynomial * L + limb (layout [B][L][N], reading C10).
-// MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat) (b_hat eval form),
-// 3: c = INTT(NTT(a) (.) NTT(b)) (b coefficient form).
-template <int LOGN, int MODE>
-__global__ void __launch_bounds__(kTeamWarps * 32)
-k_team(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
-       const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
-       uint32_t L, uint64_t units) {
-  using C = TeamCfg<LOGN>;
-  extern __shared__ __align__(16) u64 smem[];
-  const int warp = threadIdx.x >> 5;
-  const int team = (threadIdx.x & 31) / C::S;
-  const int lane = threadIdx.x & (C::S - 1);
-  const uint64_t u = ((uint64_t)blockIdx.x * kTeamWarps + warp) * C::TEAMS + team;
-  const bool active = u < units;
-  const uint64_t uu = active ? u : units - 1;   // inactive teams shadow a valid unit, never store
-  const uint32_t l = (uint32_t)(uu % L);
-  const u64 q = lc[l].q, q2 = lc[l].q2;
-  u64* buf = smem + (size_t)((warp * C::TEAMS + team) * (MODE == 3 ? 2 : 1)) * C::N;
-  const u64* src = in + uu * C::N;
-  u64 x[C::E];
+// Geometry of group G (0 .. 1024/2^K - 1) of a pass covering stages [S, S+K):
+// element j = hi 2^{n-S} + lo + i 2^{n-S-K} of polynomial `poly` in the warp.
+template <int LOGN, int S, int K>
+struct PassGeo {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int R = 1 << K;
+  static constexpr int LO = 1 << (LOGN - S - K);   // element stride inside a group
+  static constexpr int GPP = N / R;                // groups per polynomial
+  static constexpr int GPL = (kWarpElems / R) / 32;
+  int poly, hi, base;                              // base = warp-buffer index of i = 0
+  __device__ __forceinline__ PassGeo(int G) {
+    poly = G / GPP;
+    const int gl = G % GPP;
+    hi = gl / LO;
+    base = poly * N + hi * (N >> S) + (gl % LO);
+  }
+};
 
-  if (MODE == 1) {
-    // inverse: bit-reversed input -> pass-2 layout
+// K CT stages on x[0 .. 2^K) of one group; twiddle w[2^{S+v} + hi 2^v + blk].
+template <int S, int K>
+__device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, u64 q, u64 q2) {
+  sfor<0, K>([&](auto V_) {
+    constexpr int v = decltype(V_)::value;
+    constexpr int half = (1 << K) >> (v + 1);
 #pragma unroll
-    for (int i = 0; i < C::E; ++i) x[i] = src[lane + C::S * i];
-    team_p1_to_p2<LOGN>(x, buf, lane);
-    const TW* Ti = tw_inv + (size_t)l * C::N;
-    team_inv_pass2<LOGN>(x, Ti, lane, q, q2);
-    team_p2_to_p1<LOGN>(x, buf, lane);
-    team_inv_pass1<LOGN>(x, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+    for (int blk = 0; blk < (1 << v); ++blk) {
+      TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
 #pragma unroll
-    for (int i = 0; i < C::E; ++i) x[i] = canon2(x[i], q);
-  } else {
-    const TW* Tf = tw_fwd + (size_t)l * C::N;
-    u64* bbuf = buf + C::N;
-    if (MODE == 3) {
-      // NTT(b) first, parked in pass-2 layout in the second team buffer.
-      const u64* bsrc = bop + (b_bcast ? (uint64_t)l : uu) * C::N;
-#pragma unroll
-      for (int i = 0; i < C::E; ++i) x[i] = bsrc[lane + C::S * i];
-      team_fwd_pass1<LOGN>(x, Tf, q, q2);
-      team_p1_to_p2<LOGN>(x, buf, lane);
-      team_fwd_pass2<LOGN>(x, Tf, lane, q, q2);
-#pragma unroll
-      for (int i = 0; i < C::E; ++i) bbuf[team_swz<LOGN>(C::E * lane + i)] = canon4(x[i], q, q2);
+      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
     }
+  });
+}
+
+// K GS stages (reverse order).  If LAST (S == 0), local stage 0 is the final
+// stage of the inverse and carries the N^{-1} (or N^{-1} R) factor.
+template <int S, int K, bool LAST>
+__device__ __forceinline__ void gs_group(u64 (&x)[1 << K], const TW* T, int hi, TW s0, TW s1, u64 q, u64 q2) {
+  sfor<0, K>([&](auto I_) {
+    constexpr int v = K - 1 - decltype(I_)::value;
+    constexpr int half = (1 << K) >> (v + 1);
+    if constexpr (LAST && v == 0) {
 #pragma unroll
-    for (int i = 0; i < C::E; ++i) x[i] = src[lane + C::S * i];
-    team_fwd_pass1<LOGN>(x, Tf, q, q2);
-    team_p1_to_p2<LOGN>(x, buf, lane);
-    if (MODE == 2) {
-      // prefetch b_hat into the (now free) team buffer, overlapping pass 2
-      const u64* bsrc = bop + (b_bcast ? (uint64_t)l : uu) * C::N;
-#pragma unroll
-      for (int i = 0; i < C::E; ++i) cp_async8(buf + team_swz<LOGN>(lane + C::S * i), bsrc + lane + C::S * i);
-    }
-    team_fwd_pass2<LOGN>(x, Tf, lane, q, q2);
-    if (MODE == 0) {
-#pragma unroll
-      for (int i = 0; i < C::E; ++i) x[i] = canon4(x[i], q, q2);
-      team_p2_to_p1<LOGN>(x, buf, lane);
+      for (int k = 0; k < half; ++k) gs_bfly_last(x[k], x[k + half], s0, s1, q, q2);
     } else {
-      const u64* bb = buf;
-      if (MODE == 2) {
-        cp_async_wait_all();
-        __syncwarp();
-      } else {
-        bb = bbuf;
+#pragma unroll
+      for (int blk = 0; blk < (1 << v); ++blk) {
+        TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
+#pragma unroll
+        for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
       }
-      const u64 qinv = lc[l].qinv;
+    }
+  });
+}
+
+// Global view of the polynomials a warp works on: polynomial p of the warp is
+// unit (u0 + p) of one limb; element jj of it lives at base + (u0+p)*stride + jj
+// (stride = L*N for the [B][L][N] layout; 0 for a broadcast operand).
+struct GView {
+  const u64* base;
+  uint64_t u0, stride, units;
+  __device__ __forceinline__ bool live(int p) const { return u0 + p < units; }
+  __device__ __forceinline__ const u64* at(int p) const { return base + (u0 + p) * stride; }
+};
+
+// Destination kinds of a pass.
+constexpr int kToBuf = 0;      // lazy values back into the warp buffer
+constexpr int kToGlobal = 1;   // canonical values to global memory
+constexpr int kToBufCanon = 2; // canonical values into the warp buffer
+
+// ---- one forward pass (CT) over the warp buffer -----------------------------
+template <int LOGN, int S, int K, bool SRC_GLOBAL, int DST>
+__device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
+  using Geo = PassGeo<LOGN, S, K>;
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int gi = 0; gi < Geo::GPL; ++gi) {
+    const Geo g(lane + 32 * gi);
+    const int jj0 = g.base - g.poly * N;
+    u64 x[1 << K];
+    if constexpr (SRC_GLOBAL) {
+      const bool live = src.live(g.poly);
+      const u64* s = src.at(g.poly) + jj0;
 #pragma unroll
-      for (int i = 0; i < C::E; ++i) x[i] = mont_mul(x[i], bb[team_swz<LOGN>(C::E * lane + i)], q, qinv);
-      __syncwarp();
-      const TW* Ti = tw_inv + (size_t)l * C::N;
-      team_inv_pass2<LOGN>(x, Ti, lane, q, q2);
-      team_p2_to_p1<LOGN>(x, buf, lane);
-      team_inv_pass1<LOGN>(x, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2);
+      for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
+    } else {
 #pragma unroll
-      for (int i = 0; i < C::E; ++i) x[i] = canon2(x[i], q);
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+    }
+    ct_group<S, K>(x, T, g.hi, q, q2);
+    if constexpr (DST == kToGlobal) {
+      if (dst.live(g.poly)) {
+        u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
+#pragma unroll
+        for (int i = 0; i < (1 << K); ++i) d[i * Geo::LO] = canon4(x[i], q, q2);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i)
+        buf[wswz(g.base + i * Geo::LO)] = DST == kToBufCanon ? canon4(x[i], q, q2) : x[i];
     }
   }
-  if (active) {
-    u64* dst = out + u * C::N;
+  __syncwarp();
+}
+
+template <int LOGN, int S, int K, bool SRC_GLOBAL, bool DST_GLOBAL, bool LAST>
+__device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
+                                         u64 q, u64 q2) {
+  using Geo = PassGeo<LOGN, S, K>;
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int gi = 0; gi < Geo::GPL; ++gi) {
+    const Geo g(lane + 32 * gi);
+    const int jj0 = g.base - g.poly * N;
+    u64 x[1 << K];
+    if constexpr (SRC_GLOBAL) {
+      const bool live = src.live(g.poly);
+      const u64* s = src.at(g.poly) + jj0;
 #pragma unroll
-    for (int i = 0; i < C::E; ++i) dst[lane + C::S * i] = x[i];
+      for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
+    } else {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+    }
+    gs_group<S, K, LAST>(x, T, g.hi, s0, s1, q, q2);
+    if constexpr (DST_GLOBAL) {
+      if (dst.live(g.poly)) {
+        u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
+#pragma unroll
+        for (int i = 0; i < (1 << K); ++i) d[i * Geo::LO] = canon2(x[i], q);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) buf[wswz(g.base + i * Geo::LO)] = x[i];
+    }
+  }
+  __syncwarp();
+}
+
+// Fused turn-around pass of the polymul: last CT pass -> (.) b_hat -> first
+// GS pass, all in registers.  b_hat comes from global memory (bview) or from
+// a second warp buffer holding canonical NTT(b) (BSRC_BUF).
+template <int LOGN, int S, int K, bool SRC_GLOBAL, bool DST_GLOBAL, bool BSRC_BUF>
+__device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
+                                          const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
+  using Geo = PassGeo<LOGN, S, K>;
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int gi = 0; gi < Geo::GPL; ++gi) {
+    const Geo g(lane + 32 * gi);
+    const int jj0 = g.base - g.poly * N;
+    u64 x[1 << K];
+    if constexpr (SRC_GLOBAL) {
+      const bool live = src.live(g.poly);
+      const u64* s = src.at(g.poly) + jj0;
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
+    } else {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+    }
+    ct_group<S, K>(x, Tf, g.hi, q, q2);
+    if constexpr (BSRC_BUF) {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bbuf[wswz(g.base + i * Geo::LO)], q, qinv);
+    } else {
+      const bool live = bview.live(g.poly);
+      const u64* b = bview.at(g.poly) + jj0;
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], live ? __ldg(b + i * Geo::LO) : 0ull, q, qinv);
+    }
+    gs_group<S, K, S == 0>(x, Ti, g.hi, s0, s1, q, q2);
+    if constexpr (DST_GLOBAL) {
+      if (dst.live(g.poly)) {
+        u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
+#pragma unroll
+        for (int i = 0; i < (1 << K); ++i) d[i * Geo::LO] = canon2(x[i], q);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) buf[wswz(g.base + i * Geo::LO)] = x[i];
+    }
+  }
+  __syncwarp();
+}
+
+// ---- full transforms on one warp buffer ---------------------------------------
+template <int LOGN, int DST>
+__device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
+  using C = WarpCfg<LOGN>;
+  if constexpr (C::NPASS == 1) {
+    fwd_pass<LOGN, 0, C::K0, true, DST>(buf, src, dst, lane, T, q, q2);
+  } else if constexpr (C::NPASS == 2) {
+    fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, C::K0, C::K1, false, DST>(buf, src, dst, lane, T, q, q2);
+  } else {
+    fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, C::K0, C::K1, false, kToBuf>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, C::K0 + C::K1, C::K2, false, DST>(buf, src, dst, lane, T, q, q2);
+  }
+}
+
+template <int LOGN>
+__device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
+                                             u64 q, u64 q2) {
+  using C = WarpCfg<LOGN>;
+  if constexpr (C::NPASS == 1) {
+    inv_pass<LOGN, 0, C::K0, true, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+  } else if constexpr (C::NPASS == 2) {
+    inv_pass<LOGN, C::K0, C::K1, true, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+  } else {
+    inv_pass<LOGN, C::K0 + C::K1, C::K2, true, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    inv_pass<LOGN, C::K0, C::K1, false, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+  }
+}
+
+template <int LOGN, bool BSRC_BUF>
+__device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
+                                             const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
+  using C = WarpCfg<LOGN>;
+  if constexpr (C::NPASS == 1) {
+    turn_pass<LOGN, 0, C::K0, true, true, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
+  } else if constexpr (C::NPASS == 2) {
+    fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    turn_pass<LOGN, C::K0, C::K1, false, false, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2,
+                                                          qinv);
+    inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+  } else {
+    fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    fwd_pass<LOGN, C::K0, C::K1, false, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    turn_pass<LOGN, C::K0 + C::K1, C::K2, false, false, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1,
+                                                                  q, q2, qinv);
+    inv_pass<LOGN, C::K0, C::K1, false, false, false>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+    inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+  }
+}
+
+// ---- kernel --------------------------------------------------------------------
+// grid = (ceil(B / (kTeamWarps * P)), L): CTA (x, l) owns polynomials
+// [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
+// (layout [B][L][N], reading C10).
+// MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(kTeamWarps * 32)
+k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
+       const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
+       uint32_t L, uint32_t B) {
+  using C = WarpCfg<LOGN>;
+  constexpr int N = C::N;
+  extern __shared__ __align__(16) u64 smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t l = blockIdx.y;
+  const uint64_t p0 = ((uint64_t)blockIdx.x * kTeamWarps + warp) * C::P;
+  if (p0 >= B) return;   // whole warp idle (warp-uniform)
+  u64* buf = smem + (size_t)warp * kWarpElems * (MODE == 3 ? 2 : 1);
+  const u64 q = lc[l].q, q2 = lc[l].q2;
+  const uint64_t stride = (uint64_t)L * N;
+  const GView src{in + (uint64_t)l * N, p0, stride, B};
+  const GView dst{out + (uint64_t)l * N, p0, stride, B};
+  const TW* Tf = tw_fwd + (size_t)l * N;
+  const TW* Ti = tw_inv + (size_t)l * N;
+  if constexpr (MODE == 0) {
+    warp_forward<LOGN, kToGlobal>(buf, src, dst, lane, Tf, q, q2);
+  } else if constexpr (MODE == 1) {
+    warp_inverse<LOGN>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+  } else {
+    const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
+    const u64 qinv = lc[l].qinv;
+    if constexpr (MODE == 3) {
+      u64* bbuf = buf + kWarpElems;
+      // canonical NTT(b) parked in the second warp buffer
+      warp_forward<LOGN, kToBufCanon>(bbuf, bview, bview, lane, Tf, q, q2);
+      warp_polymul<LOGN, true>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+    } else {
+      warp_polymul<LOGN, false>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
+                                qinv);
+    }
   }
 }
 
 template <int LOGN, int MODE>
-inline size_t team_smem_bytes() {
-  return (size_t)kTeamWarps * TeamCfg<LOGN>::TEAMS * TeamCfg<LOGN>::N * 8 * (MODE == 3 ? 2 : 1);
+inline size_t warp_smem_bytes() {
+  return (size_t)kTeamWarps * kWarpElems * 8 * (MODE == 3 ? 2 : 1);
 }
 
 }  // namespace rnt

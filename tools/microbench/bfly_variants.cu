@@ -1,0 +1,229 @@
+// Butterfly arithmetic variants for sm_100a: throughput (bfly/clk/SM) and a
+// correctness check (results agree mod q with an exact __int128 host model).
+//
+//   V0  nvcc default: __umul64hi Shoup + csub            (baseline)
+//   V2  hand-split exact Shoup: 1 IMAD.HI + 5 IMAD.WIDE + 4 IMAD, r = YW + Q(-q)
+//   V3  V2 with a high-word-only lazy compare (range [0, 4q + 2^32))
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+typedef unsigned long long u64;
+typedef unsigned __int128 u128;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+
+struct TW { u64 w, wp; };
+
+__device__ __forceinline__ uint32_t lo32(u64 x) { return (uint32_t)x; }
+__device__ __forceinline__ uint32_t hi32(u64 x) { return (uint32_t)(x >> 32); }
+__device__ __forceinline__ u64 mwide(uint32_t a, uint32_t b, u64 c) {
+  u64 d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t mhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t mlo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ u64 pack(uint32_t lo, uint32_t hi) { return ((u64)hi << 32) | lo; }
+
+// exact hi64(y * wp) for y < 2^62 (y1 < 2^30)
+__device__ __forceinline__ u64 hi64_exact(u64 y, u64 wp) {
+  uint32_t y0 = lo32(y), y1 = hi32(y), p0 = lo32(wp), p1 = hi32(wp);
+  uint32_t A = mhi(y0, p0);
+  u64 B = mwide(y0, p1, (u64)A);            // < 2^64
+  u64 C = mwide(y1, p0, (u64)lo32(B));      // < 2^62 + 2^32
+  u64 F = (u64)hi32(B) + (u64)hi32(C);      // 64-bit add (ALU)
+  return mwide(y1, p1, F);
+}
+
+// r = y*w - Q*q (mod 2^64) with nq = -q mod 2^64
+__device__ __forceinline__ u64 shoup_r(u64 y, u64 w, u64 Q, u64 nq) {
+  uint32_t y0 = lo32(y), y1 = hi32(y), w0 = lo32(w), w1 = hi32(w);
+  u64 yw = mwide(y0, w0, 0ull);
+  uint32_t h = mlo(y0, w1, hi32(yw));
+  h = mlo(y1, w0, h);
+  yw = pack(lo32(yw), h);
+  uint32_t Q0 = lo32(Q), Q1 = hi32(Q), n0 = lo32(nq), n1 = hi32(nq);
+  u64 r = mwide(Q0, n0, yw);
+  uint32_t rh = mlo(Q0, n1, hi32(r));
+  rh = mlo(Q1, n0, rh);
+  return pack(lo32(r), rh);
+}
+
+__device__ __forceinline__ void bfly_v0(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
+  u64 x = X >= q2 ? X - q2 : X;
+  u64 Q = __umul64hi(Y, wp);
+  u64 T = Y * w - Q * q;
+  X = x + T;
+  Y = x - T + q2;
+}
+
+__device__ __forceinline__ void bfly_v2(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
+  u64 x = X >= q2 ? X - q2 : X;
+  u64 Q = hi64_exact(Y, wp);
+  u64 T = shoup_r(Y, w, Q, nq);
+  X = x + T;
+  Y = x - T + q2;
+}
+
+// high-word lazy compare: X in [0, 4q + 2^32) -> x in [0, 2q + 2^32)
+__device__ __forceinline__ void bfly_v3(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
+  u64 sub = hi32(X) > hi32(q2) ? q2 : 0ull;
+  u64 Q = hi64_exact(Y, wp);
+  u64 T = shoup_r(Y, w, Q, nq);
+  u64 x = X - sub;
+  X = x + T;
+  Y = x - T + q2;
+}
+
+
+// V4: whole CT butterfly in one PTX block (32-bit registers, explicit carries)
+__device__ __forceinline__ void bfly_v4(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
+  uint32_t x0 = lo32(X), x1 = hi32(X), y0 = lo32(Y), y1 = hi32(Y);
+  uint32_t X0, X1, Y0, Y1;
+  asm("{\n\t"
+      ".reg .u32 A, Bl, Bh, Cl, Ch, f0, f1, Q0, Q1, W0, W1, R0, R1, d0, d1, s0, s1, t0, t1;\n\t"
+      ".reg .u64 B, C, F, Q, YW, R, A64, Bl64;\n\t"
+      ".reg .pred p;\n\t"
+      "mul.hi.u32 A, %4, %8;\n\t"
+      "mov.b64 A64, {A, 0};\n\t"
+      "mad.wide.u32 B, %4, %9, A64;\n\t"
+      "mov.b64 {Bl, Bh}, B;\n\t"
+      "mov.b64 Bl64, {Bl, 0};\n\t"
+      "mad.wide.u32 C, %5, %8, Bl64;\n\t"
+      "mov.b64 {Cl, Ch}, C;\n\t"
+      "add.cc.u32 f0, Bh, Ch;\n\t"
+      "addc.u32 f1, 0, 0;\n\t"
+      "mov.b64 F, {f0, f1};\n\t"
+      "mad.wide.u32 Q, %5, %9, F;\n\t"
+      "mov.b64 {Q0, Q1}, Q;\n\t"
+      "mul.wide.u32 YW, %4, %6;\n\t"
+      "mov.b64 {W0, W1}, YW;\n\t"
+      "mad.lo.u32 W1, %4, %7, W1;\n\t"
+      "mad.lo.u32 W1, %5, %6, W1;\n\t"
+      "mov.b64 YW, {W0, W1};\n\t"
+      "mad.wide.u32 R, Q0, %10, YW;\n\t"
+      "mov.b64 {R0, R1}, R;\n\t"
+      "mad.lo.u32 R1, Q0, %11, R1;\n\t"
+      "mad.lo.u32 R1, Q1, %10, R1;\n\t"
+      // x' = X >= 2q ? X - 2q : X   (sign of the 64-bit difference)
+      "sub.cc.u32 d0, %14, %12;\n\t"
+      "subc.u32 d1, %15, %13;\n\t"
+      "setp.lt.s32 p, d1, 0;\n\t"
+      "selp.u32 d0, %14, d0, p;\n\t"
+      "selp.u32 d1, %15, d1, p;\n\t"
+      // X_out = x' + T ; Y_out = x' + 2q - T
+      "add.cc.u32 %0, d0, R0;\n\t"
+      "addc.u32 %1, d1, R1;\n\t"
+      "sub.cc.u32 t0, %12, R0;\n\t"
+      "subc.u32 t1, %13, R1;\n\t"
+      "add.cc.u32 %2, d0, t0;\n\t"
+      "addc.u32 %3, d1, t1;\n\t"
+      "}"
+      : "=r"(X0), "=r"(X1), "=r"(Y0), "=r"(Y1)
+      : "r"(y0), "r"(y1), "r"(lo32(w)), "r"(hi32(w)), "r"(lo32(wp)), "r"(hi32(wp)),
+        "r"(lo32(nq)), "r"(hi32(nq)), "r"(lo32(q2)), "r"(hi32(q2)), "r"(x0), "r"(x1));
+  X = pack(X0, X1);
+  Y = pack(Y0, Y1);
+}
+
+constexpr int ITERS = 256;
+
+template <int V>
+__global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long* cyc) {
+  u64 X[4], Y[4];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < 4; ++i) { X[i] = in[gid * 8 + 2 * i]; Y[i] = in[gid * 8 + 2 * i + 1]; }
+  const u64 q2 = 2 * q, nq = 0ull - q;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (V == 0) bfly_v0(X[i], Y[i], w, wp, q, q2, nq);
+      if (V == 2) bfly_v2(X[i], Y[i], w, wp, q, q2, nq);
+      if (V == 3) bfly_v3(X[i], Y[i], w, wp, q, q2, nq);
+      if (V == 4) bfly_v4(X[i], Y[i], w, wp, q, q2, nq);
+    }
+  }
+  long long t1 = clock64();
+  for (int i = 0; i < 4; ++i) { out[gid * 8 + 2 * i] = X[i]; out[gid * 8 + 2 * i + 1] = Y[i]; }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+static u64 mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int TPB = 256, CPS = 4, grid = sms * CPS, nthr = grid * TPB;
+  const u64 q = 1152921504606584833ull;  // 2^60 - 2^18 + 1
+  const u64 w = 987654321987654321ull % q;
+  const u64 wp = (u64)(((u128)w << 64) / q);
+  u64 *din, *dout;
+  long long* cyc;
+  CK(cudaMalloc(&din, (size_t)nthr * 8 * 8));
+  CK(cudaMalloc(&dout, (size_t)nthr * 8 * 8));
+  CK(cudaMalloc(&cyc, grid * 8));
+  u64* h = (u64*)malloc((size_t)nthr * 8 * 8);
+  u64* ho = (u64*)malloc((size_t)nthr * 8 * 8);
+  u64 s = 88172645463325252ull;
+  for (size_t i = 0; i < (size_t)nthr * 8; ++i) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; h[i] = s % q; }
+  CK(cudaMemcpy(din, h, (size_t)nthr * 64, cudaMemcpyHostToDevice));
+  long long* hc = (long long*)malloc(grid * 8);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  // host reference for 8 threads' worth of pairs
+  const int NREF = 64;
+  u64 refX[NREF], refY[NREF];
+  for (int i = 0; i < NREF; ++i) {
+    u64 X = h[2 * i], Y = h[2 * i + 1];
+    for (int it = 0; it < ITERS; ++it) {
+      u64 t = mulmod(Y, w, q);
+      u64 nx = (X + t) % q, ny = (X + q - t) % q;
+      X = nx; Y = ny;
+    }
+    refX[i] = X; refY[i] = Y;
+  }
+  auto run = [&](auto kern, const char* name) {
+    kern<<<grid, TPB>>>(dout, din, w, wp, q, cyc);
+    cudaEventRecord(e0);
+    kern<<<grid, TPB>>>(dout, din, w, wp, q, cyc);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    CK(cudaMemcpy(hc, cyc, grid * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ho, dout, (size_t)nthr * 64, cudaMemcpyDeviceToHost));
+    long long mx = 0; double avg = 0;
+    for (int i = 0; i < grid; ++i) { if (hc[i] > mx) mx = hc[i]; avg += hc[i]; }
+    avg /= grid;
+    int bad = 0;
+    for (int i = 0; i < NREF; ++i) {
+      // thread t = i/4 pair k = i%4 -> positions t*8 + 2k
+      int t = i / 4, k = i % 4;
+      u64 X = ho[t * 8 + 2 * k] % q, Y = ho[t * 8 + 2 * k + 1] % q;
+      u64 hX = h[t * 8 + 2 * k], hY = h[t * 8 + 2 * k + 1];
+      u64 rX = hX, rY = hY;
+      for (int it = 0; it < ITERS; ++it) { u64 tt = mulmod(rY, w, q); u64 nx = (rX + tt) % q, ny = (rX + q - tt) % q; rX = nx; rY = ny; }
+      if (X != rX || Y != rY) ++bad;
+    }
+    double bfly_sm = (double)ITERS * 4 * TPB * CPS;
+    printf("{\"variant\":\"%s\",\"bfly_per_clk_per_sm\":%.3f,\"avg_cyc_basis\":%.3f,\"ms\":%.4f,\"mhz\":%.0f,\"bad\":%d}\n",
+           name, bfly_sm / mx, bfly_sm / avg, ms, mx / (ms * 1e3), bad);
+  };
+  for (int rep = 0; rep < 2; ++rep) {
+    run(k_bfly<0>, "V0_nvcc");
+    run(k_bfly<2>, "V2_split_exact");
+    run(k_bfly<3>, "V3_split_hiword");
+    run(k_bfly<4>, "V4_ptx_block");
+  }
+  (void)refX; (void)refY;
+  return 0;
+}
