@@ -253,11 +253,25 @@ def bench_ours(args, wl, parts):
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
-    # ---- shard: weak scaling -> rank r owns global polynomial block r.
+    # ---- shard.  weak: rank r owns global polynomial block r of every part.
+    # strong: the fixed global job is split by limb x polynomial with the
+    # weighted contiguous planner of SURVEY §8(e) (paper_2410_05934_b200.shard).
+    from paper_2410_05934_b200 import shard as shd
+
+    blocks = []   # (log2n, limbs_slice_mods, limb_offset, total_limbs, polys, poly_offset, seed)
+    if args.scaling == "weak":
+        for (logn, limbs, polys, seed) in parts:
+            blocks.append((logn, primes_for(logn, limbs), 0, limbs, polys, rank * polys, seed))
+    else:
+        sp = [shd.Part(lg, lm, po) for (lg, lm, po, _) in parts]
+        for b in shd.plan(sp, ws)[rank]:
+            logn, limbs, polys, seed = parts[b.part]
+            mods = primes_for(logn, limbs)[b.limb_begin:b.limb_end]
+            blocks.append((logn, mods, b.limb_begin, limbs, b.poly_end - b.poly_begin, b.poly_begin, seed))
     states = []
-    for (logn, limbs, polys, seed) in parts:
-        off = rank * polys if args.scaling == "weak" else 0
-        mods, a, bhat = make_part_inputs(logn, limbs, polys, seed, off)
+    for (logn, mods, loff, ltot, polys, poff, seed) in blocks:
+        a = inputs.residues_limbs(seed, polys, mods, 1 << logn, loff, ltot, batch_offset=poff)
+        bhat = inputs.residues_limbs(seed + 1, polys, mods, 1 << logn, loff, ltot, batch_offset=poff)
         plan = R.Plan(logn, mods, device=local)
         da = torch.from_numpy(a.view(np.int64)).to(dev)
         db = torch.from_numpy(bhat.view(np.int64)).to(dev)
@@ -265,11 +279,11 @@ def bench_ours(args, wl, parts):
         ha = torch.from_numpy(a.view(np.int64)).pin_memory()
         hc = torch.empty_like(ha).pin_memory()
         ws_buf = torch.empty_like(da)
-        states.append(dict(logn=logn, limbs=limbs, polys=polys, plan=plan, a=da, b=db, c=dc,
+        states.append(dict(logn=logn, limbs=len(mods), polys=polys, plan=plan, a=da, b=db, c=dc,
                            ha=ha, hc=hc, ws=ws_buf))
     # the dominant kernel: largest butterfly count part
     work = [(2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]) for s in states]
-    dom = int(np.argmax(work))
+    dom = int(np.argmax(work)) if work else 0
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step(ev=None):
@@ -329,9 +343,10 @@ def bench_ours(args, wl, parts):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     total_ms, e2e_ms = float(t[0]), float(t[1])
 
-    per_rank = transforms_per_step(parts)
-    value = per_rank * ws * args.steps / (total_ms * 1e-3)
-    e2e_value = per_rank * ws * args.steps / (e2e_ms * 1e-3)
+    # units all ranks processed per step: weak = ws copies of the workload, strong = one
+    global_xf = transforms_per_step(parts) * (ws if args.scaling == "weak" else 1)
+    value = global_xf * args.steps / (total_ms * 1e-3)
+    e2e_value = global_xf * args.steps / (e2e_ms * 1e-3)
 
     # ---- roofline of the dominant kernel(s)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -398,7 +413,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -85,29 +86,54 @@ static int num_sms() {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE>
-static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
-                              int bcast, uint32_t batch, cudaStream_t st) {
+template <int LOGN, int MODE, int W, int MINB, bool SYNC>
+static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
+                                int bcast, uint32_t batch, cudaStream_t st) {
   static bool attr_set = false;  // benign race: idempotent attribute call
-  const size_t smem = warp_smem_bytes<LOGN, MODE>();
+  const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
   if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE, W, MINB, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr_set = true;
   }
-  const uint64_t per_cta = (uint64_t)kTeamWarps * WarpCfg<LOGN>::P;
+  const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    // limb offset l0: shift every per-limb base pointer
-    k_warp<LOGN, MODE><<<grid, kTeamWarps * 32, smem, st>>>(out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN),
-                                                           bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
-                                                           p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN),
-                                                           p->d_lc + l0, p->L, batch);
+    k_warp<LOGN, MODE, W, MINB, SYNC><<<grid, W * 32, smem, st>>>(
+        out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
+        p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
   return RNT_OK;
+}
+
+// Tuning knob (benchmarks only): RNT_SMALL_VARIANT selects the N=2^10 launch
+// configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
+static int small_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RNT_SMALL_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int LOGN, int MODE>
+static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
+                              int bcast, uint32_t batch, cudaStream_t st) {
+  if constexpr (LOGN == 10 && MODE != 3) {
+    switch (small_variant()) {
+      case 1: return launch_warp_v<LOGN, MODE, 4, 5, false>(p, out, in, bop, bcast, batch, st);
+      case 2: return launch_warp_v<LOGN, MODE, 16, 1, true>(p, out, in, bop, bcast, batch, st);
+      case 3: return launch_warp_v<LOGN, MODE, 8, 2, true>(p, out, in, bop, bcast, batch, st);
+      case 4: return launch_warp_v<LOGN, MODE, 20, 1, true>(p, out, in, bop, bcast, batch, st);
+      default: break;
+    }
+  }
+  return launch_warp_v<LOGN, MODE, kTeamWarps, 1, false>(p, out, in, bop, bcast, batch, st);
 }
 
 template <int MODE>

@@ -16,8 +16,8 @@
 //     layout) and the last pass of each direction writes global memory;
 //   * polymul fuses last-forward-pass -> (.) b_hat -> first-inverse-pass in
 //     registers (the NTT-domain product never touches shared memory);
-//   * shared-memory index swizzle j ^ ((j >> 4) & 15) makes all three pass
-//     patterns of N = 2^10 conflict-free.
+//   * shared-memory padding j + (j >> 4) makes all three pass patterns of
+//     N = 2^10 conflict-free with immediate-offset addressing (wpad).
 // Lazy Harvey ranges (modarith.cuh); outputs are canonical.
 #pragma once
 #include "modarith.cuh"
@@ -38,7 +38,17 @@ struct WarpCfg {
   static_assert(K2 <= 4, "N <= 2^12");
 };
 
-__device__ __forceinline__ int wswz(int j) { return j ^ ((j >> 4) & 15); }
+// Shared-memory layout of a warp buffer: one pad word per 16 coefficients,
+// phys(j) = j + (j >> 4).  For N = 2^10 every pass pattern (group stride 64,
+// 4 and 1) is bank-conflict free, and inside a group the offsets
+// phys(base + i LO) - phys(base) are compile-time constants (pad_off), so
+// each shared access is one LDS/STS with an immediate offset.
+constexpr int kWarpBuf = kWarpElems + kWarpElems / 16;
+__device__ __forceinline__ int wpad(int j) { return j + (j >> 4); }
+template <int LOGN, int S, int LO>
+__host__ __device__ constexpr int pad_off(int i) {
+  return ((1 << (LOGN - S)) >= 16) ? i * LO + ((i * LO) >> 4) : i * LO;
+}
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -124,6 +134,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
   for (int gi = 0; gi < Geo::GPL; ++gi) {
     const Geo g(lane + 32 * gi);
     const int jj0 = g.base - g.poly * N;
+    const int pb = wpad(g.base);
     u64 x[1 << K];
     if constexpr (SRC_GLOBAL) {
       const bool live = src.live(g.poly);
@@ -132,7 +143,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
     } else {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
     ct_group<S, K>(x, T, g.hi, q, q2);
     if constexpr (DST == kToGlobal) {
@@ -144,7 +155,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
     } else {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i)
-        buf[wswz(g.base + i * Geo::LO)] = DST == kToBufCanon ? canon4(x[i], q, q2) : x[i];
+        buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = DST == kToBufCanon ? canon4(x[i], q, q2) : x[i];
     }
   }
   __syncwarp();
@@ -159,6 +170,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
   for (int gi = 0; gi < Geo::GPL; ++gi) {
     const Geo g(lane + 32 * gi);
     const int jj0 = g.base - g.poly * N;
+    const int pb = wpad(g.base);
     u64 x[1 << K];
     if constexpr (SRC_GLOBAL) {
       const bool live = src.live(g.poly);
@@ -167,7 +179,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
     } else {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
     gs_group<S, K, LAST>(x, T, g.hi, s0, s1, q, q2);
     if constexpr (DST_GLOBAL) {
@@ -178,7 +190,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) buf[wswz(g.base + i * Geo::LO)] = x[i];
+      for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
     }
   }
   __syncwarp();
@@ -196,6 +208,7 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
   for (int gi = 0; gi < Geo::GPL; ++gi) {
     const Geo g(lane + 32 * gi);
     const int jj0 = g.base - g.poly * N;
+    const int pb = wpad(g.base);
     u64 x[1 << K];
     if constexpr (SRC_GLOBAL) {
       const bool live = src.live(g.poly);
@@ -204,12 +217,12 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
     } else {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = buf[wswz(g.base + i * Geo::LO)];
+      for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
     ct_group<S, K>(x, Tf, g.hi, q, q2);
     if constexpr (BSRC_BUF) {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bbuf[wswz(g.base + i * Geo::LO)], q, qinv);
+      for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bbuf[pb + pad_off<LOGN, S, Geo::LO>(i)], q, qinv);
     } else {
       const bool live = bview.live(g.poly);
       const u64* b = bview.at(g.poly) + jj0;
@@ -225,62 +238,83 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) buf[wswz(g.base + i * Geo::LO)] = x[i];
+      for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
     }
   }
   __syncwarp();
 }
 
 // ---- full transforms on one warp buffer ---------------------------------------
-template <int LOGN, int DST>
+template <int LOGN, int DST, bool SYNC = false>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using C = WarpCfg<LOGN>;
   if constexpr (C::NPASS == 1) {
     fwd_pass<LOGN, 0, C::K0, true, DST>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
   } else if constexpr (C::NPASS == 2) {
     fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
     fwd_pass<LOGN, C::K0, C::K1, false, DST>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
   } else {
     fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
     fwd_pass<LOGN, C::K0, C::K1, false, kToBuf>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
     fwd_pass<LOGN, C::K0 + C::K1, C::K2, false, DST>(buf, src, dst, lane, T, q, q2);
+    if constexpr (SYNC) __syncthreads();
   }
 }
 
-template <int LOGN>
+template <int LOGN, bool SYNC = false>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
   using C = WarpCfg<LOGN>;
   if constexpr (C::NPASS == 1) {
     inv_pass<LOGN, 0, C::K0, true, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
   } else if constexpr (C::NPASS == 2) {
     inv_pass<LOGN, C::K0, C::K1, true, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
   } else {
     inv_pass<LOGN, C::K0 + C::K1, C::K2, true, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, C::K0, C::K1, false, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
   }
 }
 
-template <int LOGN, bool BSRC_BUF>
+template <int LOGN, bool BSRC_BUF, bool SYNC = false>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using C = WarpCfg<LOGN>;
   if constexpr (C::NPASS == 1) {
     turn_pass<LOGN, 0, C::K0, true, true, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
+    if constexpr (SYNC) __syncthreads();
   } else if constexpr (C::NPASS == 2) {
     fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    if constexpr (SYNC) __syncthreads();
     turn_pass<LOGN, C::K0, C::K1, false, false, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2,
                                                           qinv);
+                                                          if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
   } else {
     fwd_pass<LOGN, 0, C::K0, true, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    if constexpr (SYNC) __syncthreads();
     fwd_pass<LOGN, C::K0, C::K1, false, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    if constexpr (SYNC) __syncthreads();
     turn_pass<LOGN, C::K0 + C::K1, C::K2, false, false, BSRC_BUF>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1,
                                                                   q, q2, qinv);
+                                                                  if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, C::K0, C::K1, false, false, false>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
     inv_pass<LOGN, 0, C::K0, false, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+    if constexpr (SYNC) __syncthreads();
   }
 }
 
@@ -289,8 +323,8 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
-template <int LOGN, int MODE>
-__global__ void __launch_bounds__(kTeamWarps * 32)
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false>
+__global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
        uint32_t L, uint32_t B) {
@@ -300,9 +334,9 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t l = blockIdx.y;
-  const uint64_t p0 = ((uint64_t)blockIdx.x * kTeamWarps + warp) * C::P;
-  if (p0 >= B) return;   // whole warp idle (warp-uniform)
-  u64* buf = smem + (size_t)warp * kWarpElems * (MODE == 3 ? 2 : 1);
+  const uint64_t p0 = ((uint64_t)blockIdx.x * W + warp) * C::P;
+  if (!SYNC && p0 >= B) return;   // whole warp idle (warp-uniform); with SYNC idle warps run predicated
+  u64* buf = smem + (size_t)warp * kWarpBuf * (MODE == 3 ? 2 : 1);
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const uint64_t stride = (uint64_t)L * N;
   const GView src{in + (uint64_t)l * N, p0, stride, B};
@@ -310,27 +344,27 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Tf = tw_fwd + (size_t)l * N;
   const TW* Ti = tw_inv + (size_t)l * N;
   if constexpr (MODE == 0) {
-    warp_forward<LOGN, kToGlobal>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<LOGN, kToGlobal, SYNC>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<LOGN>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+    warp_inverse<LOGN, SYNC>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
   } else {
     const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
     const u64 qinv = lc[l].qinv;
     if constexpr (MODE == 3) {
-      u64* bbuf = buf + kWarpElems;
+      u64* bbuf = buf + kWarpBuf;
       // canonical NTT(b) parked in the second warp buffer
-      warp_forward<LOGN, kToBufCanon>(bbuf, bview, bview, lane, Tf, q, q2);
-      warp_polymul<LOGN, true>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+      warp_forward<LOGN, kToBufCanon, SYNC>(bbuf, bview, bview, lane, Tf, q, q2);
+      warp_polymul<LOGN, true, SYNC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     } else {
-      warp_polymul<LOGN, false>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
+      warp_polymul<LOGN, false, SYNC>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
                                 qinv);
     }
   }
 }
 
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, int W = kTeamWarps>
 inline size_t warp_smem_bytes() {
-  return (size_t)kTeamWarps * kWarpElems * 8 * (MODE == 3 ? 2 : 1);
+  return (size_t)W * kWarpBuf * 8 * (MODE == 3 ? 2 : 1);
 }
 
 }  // namespace rnt

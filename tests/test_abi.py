@@ -84,3 +84,16 @@ def test_null_plan_calls(lib):
     assert _lib.L.rnt_ntt_forward(None, None, None, 1, None) == lib.RNT_E_INVALID_ARG
     assert _lib.L.rnt_polymul(None, None, None, None, 1, 0, 0, None) == lib.RNT_E_INVALID_ARG
     assert _lib.L.rnt_plan_destroy(None) == lib.RNT_OK
+
+
+def test_product_path_never_touches_oracle():
+    """The product package must not import, link or call oracle/ (test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_2410_05934_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "ntt_oracle" not in src and "liboracle" not in src, f
+    hdr = open(HDR).read()
+    assert "oracle" not in hdr

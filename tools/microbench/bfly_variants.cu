@@ -136,6 +136,107 @@ __device__ __forceinline__ void bfly_v4(u64& X, u64& Y, u64 w, u64 wp, u64 q, u6
   Y = pack(Y0, Y1);
 }
 
+
+// V5: approximate Shoup quotient (lo partials dropped, Q' in [Qe-2, Qe] ->
+// r in [0, 4q)), lazy invariant [0, 8q + 2^32), high-word compare.  q < 2^60.
+__device__ __forceinline__ void bfly_v5(u64& X, u64& Y, u64 w, u64 wp, u64 q4, u64 nq) {
+  const uint32_t y0 = lo32(Y), y1 = hi32(Y);
+  const uint32_t p0 = lo32(wp), p1 = hi32(wp), w0 = lo32(w), w1 = hi32(w);
+  u64 B, C, S, Q, YW, R;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(B) : "r"(y0), "r"(p1));
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(C) : "r"(y1), "r"(p0));
+  S = (u64)hi32(B) + (u64)hi32(C);
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(Q) : "r"(y1), "r"(p1), "l"(S));
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(YW) : "r"(y0), "r"(w0));
+  uint32_t h = hi32(YW);
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(y0), "r"(w1));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(y1), "r"(w0));
+  YW = pack(lo32(YW), h);
+  const uint32_t Q0 = lo32(Q), Q1 = hi32(Q);
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(R) : "r"(Q0), "r"(lo32(nq)), "l"(YW));
+  uint32_t rh = hi32(R);
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(rh) : "r"(Q0), "r"(hi32(nq)));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(rh) : "r"(Q1), "r"(lo32(nq)));
+  const u64 r = pack(lo32(R), rh);
+  const bool big = hi32(X) > hi32(q4);
+  const u64 sub = big ? q4 : 0ull;
+  const u64 add = big ? 0ull : q4;
+  const u64 Xin = X;
+  X = Xin - sub + r;
+  Y = Xin + add - r;
+}
+
+// V6: exact Shoup with a 3-input carry sum (IMAD.HI + 3 WIDE + IADD3 chain).
+__device__ __forceinline__ void bfly_v6(u64& X, u64& Y, u64 w, u64 wp, u64 q2, u64 nq) {
+  const uint32_t y0 = lo32(Y), y1 = hi32(Y);
+  const uint32_t p0 = lo32(wp), p1 = hi32(wp), w0 = lo32(w), w1 = hi32(w);
+  u64 B, C, D, YW, R;
+  uint32_t A, t0, t1, s;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(A) : "r"(y0), "r"(p0));
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(B) : "r"(y0), "r"(p1));
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(C) : "r"(y1), "r"(p0));
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(D) : "r"(y1), "r"(p1));
+  asm("{\n\t"
+      "add.cc.u32 %2, %3, %4;\n\t"
+      "addc.cc.u32 %0, %5, %6;\n\t"
+      "addc.u32 %1, %7, 0;\n\t"
+      "add.cc.u32 %2, %2, %8;\n\t"
+      "addc.cc.u32 %0, %0, %9;\n\t"
+      "addc.u32 %1, %1, 0;\n\t"
+      "}"
+      : "=r"(t0), "=r"(t1), "=r"(s)
+      : "r"(lo32(B)), "r"(lo32(C)), "r"(lo32(D)), "r"(hi32(B)), "r"(hi32(D)), "r"(A), "r"(hi32(C)));
+  const uint32_t Q0 = t0, Q1 = t1;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(YW) : "r"(y0), "r"(w0));
+  uint32_t h = hi32(YW);
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(y0), "r"(w1));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(y1), "r"(w0));
+  YW = pack(lo32(YW), h);
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(R) : "r"(Q0), "r"(lo32(nq)), "l"(YW));
+  uint32_t rh = hi32(R);
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(rh) : "r"(Q0), "r"(hi32(nq)));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(rh) : "r"(Q1), "r"(lo32(nq)));
+  const u64 r = pack(lo32(R), rh);
+  const bool big = hi32(X) > hi32(q2);
+  const u64 sub = big ? q2 : 0ull;
+  const u64 add = big ? 0ull : q2;
+  const u64 Xin = X;
+  X = Xin - sub + r;
+  Y = Xin + add - r;
+}
+
+
+// V7: nvcc-style C, but T = Y*w + Q*(-q) (negation folded into the constant)
+//     and a high-word-only lazy compare.
+__device__ __forceinline__ void bfly_v7(u64& X, u64& Y, u64 w, u64 wp, u64 q2, u64 nq) {
+  const u64 Q = __umul64hi(Y, wp);
+  const u64 T = Y * w + Q * nq;
+  const bool big = (uint32_t)(X >> 32) > (uint32_t)(q2 >> 32);
+  const u64 x = X - (big ? q2 : 0ull);
+  X = x + T;
+  Y = x + q2 - T;
+}
+// V8: V7 with the approximate quotient (r in [0,4q)), invariant [0, 8q + 2^32).
+__device__ __forceinline__ void bfly_v8(u64& X, u64& Y, u64 w, u64 wp, u64 q4, u64 nq) {
+  const uint32_t y0 = (uint32_t)Y, y1 = (uint32_t)(Y >> 32), p0 = (uint32_t)wp, p1 = (uint32_t)(wp >> 32);
+  const u64 Q = (u64)y1 * p1 + (((u64)y0 * p1) >> 32) + (((u64)y1 * p0) >> 32);
+  const u64 T = Y * w + Q * nq;
+  const bool big = (uint32_t)(X >> 32) > (uint32_t)(q4 >> 32);
+  const u64 x = X - (big ? q4 : 0ull);
+  X = x + T;
+  Y = x + q4 - T;
+}
+// V9: V8 but with __umulhi for the two cross terms.
+__device__ __forceinline__ void bfly_v9(u64& X, u64& Y, u64 w, u64 wp, u64 q4, u64 nq) {
+  const uint32_t y0 = (uint32_t)Y, y1 = (uint32_t)(Y >> 32), p0 = (uint32_t)wp, p1 = (uint32_t)(wp >> 32);
+  const u64 Q = (u64)y1 * p1 + (u64)__umulhi(y0, p1) + (u64)__umulhi(y1, p0);
+  const u64 T = Y * w + Q * nq;
+  const bool big = (uint32_t)(X >> 32) > (uint32_t)(q4 >> 32);
+  const u64 x = X - (big ? q4 : 0ull);
+  X = x + T;
+  Y = x + q4 - T;
+}
+
 constexpr int ITERS = 256;
 
 template <int V>
@@ -152,6 +253,11 @@ __global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long*
       if (V == 2) bfly_v2(X[i], Y[i], w, wp, q, q2, nq);
       if (V == 3) bfly_v3(X[i], Y[i], w, wp, q, q2, nq);
       if (V == 4) bfly_v4(X[i], Y[i], w, wp, q, q2, nq);
+      if (V == 5) bfly_v5(X[i], Y[i], w, wp, 4 * q, nq);
+      if (V == 6) bfly_v6(X[i], Y[i], w, wp, q2, nq);
+      if (V == 7) bfly_v7(X[i], Y[i], w, wp, q2, nq);
+      if (V == 8) bfly_v8(X[i], Y[i], w, wp, 4 * q, nq);
+      if (V == 9) bfly_v9(X[i], Y[i], w, wp, 4 * q, nq);
     }
   }
   long long t1 = clock64();
@@ -223,6 +329,11 @@ int main() {
     run(k_bfly<2>, "V2_split_exact");
     run(k_bfly<3>, "V3_split_hiword");
     run(k_bfly<4>, "V4_ptx_block");
+    run(k_bfly<5>, "V5_approxQ_8q");
+    run(k_bfly<6>, "V6_exact_carry3");
+    run(k_bfly<7>, "V7_c_nq_hiword");
+    run(k_bfly<8>, "V8_c_approx");
+    run(k_bfly<9>, "V9_c_approx_umulhi");
   }
   (void)refX; (void)refY;
   return 0;
