@@ -114,7 +114,7 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period: float = 0.05):
+    def __init__(self, index: int, period: float = 0.0):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -141,7 +141,8 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(self.period)
+            if self.period:
+                time.sleep(self.period)
 
     def __enter__(self):
         if self._nv is not None:
@@ -364,8 +365,8 @@ def bench_ours(args, wl, parts):
             traffic = json.load(open(prof)).get(f"{wl}:part{dom}")
         except Exception:
             traffic = None
-    kern = "k_team<10,2> (fused NTT->(.)->INTT, N=2^10)" if s["logn"] <= 10 else \
-        "k_col_fwd + k_row<16,2> + k_col_inv (N=2^16 polymul)"
+    kern = f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch)" if s["logn"] <= 10 else \
+        f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
     roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak_bfly,
             "unit": "Gbutterfly/s", "frac": achieved / peak_bfly, "traffic": traffic,
             "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
@@ -409,7 +410,7 @@ def bench_ours(args, wl, parts):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -121,19 +121,50 @@ static int small_variant() {
   return v;
 }
 
+template <int LOGN, int MODE, int W>
+static rnt_status launch_warp_tma(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                  uint32_t batch, cudaStream_t st) {
+  static int max_ctas_per_sm = 0;  // benign race: idempotent
+  const size_t smem = warp_tma_smem_bytes<W>();
+  if (!max_ctas_per_sm) {
+    RNT_CUDA(cudaFuncSetAttribute(k_warp_tma<LOGN, MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int n = 0;
+    RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_warp_tma<LOGN, MODE, W>, W * 32, smem));
+    max_ctas_per_sm = n > 0 ? n : 1;
+  }
+  // persistent grid: as many warps as fit, then shrink so every warp runs the
+  // same number of iterations (no tail imbalance).
+  const uint64_t groups = ((uint64_t)batch + WarpCfg<LOGN>::P - 1) / WarpCfg<LOGN>::P;
+  for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
+    const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
+    uint64_t max_warps = (uint64_t)num_sms() * max_ctas_per_sm * W / nl;
+    if (max_warps < W) max_warps = W;
+    const uint64_t iters = (groups + max_warps - 1) / max_warps;
+    const uint64_t warps = (groups + iters - 1) / iters;
+    dim3 grid((unsigned)((warps + W - 1) / W), nl);
+    k_warp_tma<LOGN, MODE, W><<<grid, W * 32, smem, st>>>(
+        out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
+        p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
+}
+
 template <int LOGN, int MODE>
 static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                               int bcast, uint32_t batch, cudaStream_t st) {
   if constexpr (LOGN == 10 && MODE != 3) {
     switch (small_variant()) {
-      case 1: return launch_warp_v<LOGN, MODE, 4, 5, false>(p, out, in, bop, bcast, batch, st);
-      case 2: return launch_warp_v<LOGN, MODE, 16, 1, true>(p, out, in, bop, bcast, batch, st);
-      case 3: return launch_warp_v<LOGN, MODE, 8, 2, true>(p, out, in, bop, bcast, batch, st);
-      case 4: return launch_warp_v<LOGN, MODE, 20, 1, true>(p, out, in, bop, bcast, batch, st);
+      case 5: return launch_warp_tma<LOGN, MODE, 4>(p, out, in, bop, bcast, batch, st);
+      case 6: return launch_warp_tma<LOGN, MODE, 2>(p, out, in, bop, bcast, batch, st);
+      case 1: return launch_warp_v<LOGN, MODE, 4, 4, false>(p, out, in, bop, bcast, batch, st);
+      case 7: return launch_warp_v<LOGN, MODE, kTeamWarps, 1, false>(p, out, in, bop, bcast, batch, st);
       default: break;
     }
   }
-  return launch_warp_v<LOGN, MODE, kTeamWarps, 1, false>(p, out, in, bop, bcast, batch, st);
+  // default: 2 warps per CTA, <= 128 registers (16 warps/SM) -- fastest measured
+  return launch_warp_v<LOGN, MODE, 2, 8, false>(p, out, in, bop, bcast, batch, st);
 }
 
 template <int MODE>
@@ -154,18 +185,50 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // CTA order for the two-pass kernels: block b -> (sub-block, poly, limb) with
 // the sub-block fastest, then the polynomial, then the limb, so CTAs that
 // share a limb's twiddle rows run back to back (L2 reuse across the batch).
-template <int LOGN>
-static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
-                             uint32_t batch, cudaStream_t st) {
+static int large_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RNT_LARGE_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int LOGN, int CT>
+static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
+                               uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
   const uint64_t units = (uint64_t)batch * p->L;
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
-    dim3 g(P::Cn / kColTile, (unsigned)cnt);
+    dim3 g(P::Cn / CT, (unsigned)cnt);
     if (inv)
-      k_col_inv<LOGN><<<g, P::P1_THREADS, 0, st>>>(out, in, p->d_col_inv, p->d_lc, p->L, batch, y0, after_mont);
+      k_col_inv<LOGN, CT><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_inv, p->d_lc, p->L, batch, y0, after_mont);
     else
-      k_col_fwd<LOGN><<<g, P::P1_THREADS, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
+      k_col_fwd<LOGN, CT><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
+}
+
+template <int LOGN>
+static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
+                             uint32_t batch, cudaStream_t st) {
+  if (large_variant() & 1) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
+  return launch_col_v<LOGN, kColTile>(p, inv, after_mont, out, in, batch, st);
+}
+
+template <int LOGN, int MODE, int RPC_>
+static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                               uint32_t batch, cudaStream_t st) {
+  using P = TwoPass<LOGN>;
+  const uint64_t units = (uint64_t)batch * p->L;
+  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
+    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
+    dim3 g(P::R / RPC_, (unsigned)cnt);
+    k_row<LOGN, MODE, RPC_><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv, p->d_lc, p->L,
+                                                       batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -175,17 +238,9 @@ static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64*
 template <int LOGN, int MODE>
 static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                              uint32_t batch, cudaStream_t st) {
-  using P = TwoPass<LOGN>;
-  const uint64_t units = (uint64_t)batch * p->L;
-  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
-    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
-    dim3 g(P::R / P::RPC, (unsigned)cnt);
-    k_row<LOGN, MODE><<<g, P::P2_THREADS, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv, p->d_lc, p->L,
-                                                  batch, y0);
-    rnt_status s = after_launch();
-    if (s != RNT_OK) return s;
-  }
-  return RNT_OK;
+  constexpr int R4 = TwoPass<LOGN>::RPC / 4 > 0 ? TwoPass<LOGN>::RPC / 4 : 1;
+  if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4>(p, out, in, bop, bcast, batch, st);
+  return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
 template <int LOGN>

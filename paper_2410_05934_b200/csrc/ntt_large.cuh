@@ -53,20 +53,20 @@ __device__ __forceinline__ int row_swz(int c) {
 // ============================== pass 1 (columns) ==============================
 // Forward: CT stages 0..n1-1 on columns [cb*16, cb*16+16) of unit u.
 // MODE 0: plain forward (in -> out).
-template <int LOGN>
-__global__ void __launch_bounds__(TwoPass<LOGN>::P1_THREADS)
+template <int LOGN, int CT = kColTile>
+__global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
 k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 tile[P::R * kColTile];
-  const int c = threadIdx.x % kColTile;
-  const int r0 = threadIdx.x / kColTile;
+  __shared__ __align__(16) u64 tile[P::R * CT];
+  const int c = threadIdx.x % CT;
+  const int r0 = threadIdx.x / CT;
   const uint64_t y = y0 + blockIdx.y;          // y = limb * B + poly (limb-major CTA order)
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const TW* T = tw_col + (size_t)l * P::R;
-  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * kColTile + c;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
   u64 x[kEl];
 #pragma unroll
   for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(r0 + P::T1 * i) * P::Cn];
@@ -82,11 +82,11 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
     }
   });
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) tile[(r0 + P::T1 * i) * kColTile + c] = x[i];
+  for (int i = 0; i < kEl; ++i) tile[(r0 + P::T1 * i) * CT + c] = x[i];
   __syncthreads();
   const int r1 = r0;
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) x[i] = tile[(kEl * r1 + i) * kColTile + c];
+  for (int i = 0; i < kEl; ++i) x[i] = tile[(kEl * r1 + i) * CT + c];
   // sub-pass B: stages 4..n1-1 on rows 16 r1 + i; twiddle w[2^s + ((16 r1 + i) >> (n1 - s))]
   sfor<4, P::n1>([&](auto S_) {
     constexpr int s = decltype(S_)::value;
@@ -103,20 +103,20 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
 }
 
 // Inverse: GS stages n1-1..0 (+ N^{-1} or N^{-1} R scaling), canonical output.
-template <int LOGN>
-__global__ void __launch_bounds__(TwoPass<LOGN>::P1_THREADS)
+template <int LOGN, int CT = kColTile>
+__global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
 k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 tile[P::R * kColTile];
-  const int c = threadIdx.x % kColTile;
-  const int r1 = threadIdx.x / kColTile;
+  __shared__ __align__(16) u64 tile[P::R * CT];
+  const int c = threadIdx.x % CT;
+  const int r1 = threadIdx.x / CT;
   const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const TW* T = tw_col + (size_t)l * P::R;
-  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * kColTile + c;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
   u64 x[kEl];
 #pragma unroll
   for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(kEl * r1 + i) * P::Cn];
@@ -131,11 +131,11 @@ k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
     }
   });
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) tile[(kEl * r1 + i) * kColTile + c] = x[i];
+  for (int i = 0; i < kEl; ++i) tile[(kEl * r1 + i) * CT + c] = x[i];
   __syncthreads();
   const int r0 = r1;
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) x[i] = tile[(r0 + P::T1 * i) * kColTile + c];
+  for (int i = 0; i < kEl; ++i) x[i] = tile[(r0 + P::T1 * i) * CT + c];
   sfor<0, 3>([&](auto I_) {
     constexpr int s = 3 - decltype(I_)::value;
     constexpr int half = kEl >> (s + 1);
@@ -244,16 +244,16 @@ __device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
 // MODE 0: forward rows (CT stages n1..n-1, canonical output)
 // MODE 1: inverse rows (GS stages n-1..n1, lazy [0,2q) output for k_col_inv)
 // MODE 2: fused forward rows -> (.) b_hat (Montgomery) -> inverse rows
-template <int LOGN, int MODE>
-__global__ void __launch_bounds__(TwoPass<LOGN>::P2_THREADS)
+template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC>
+__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2)
 k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
       const TW* __restrict__ tw_row_fwd, const TW* __restrict__ tw_row_inv,
       const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 sbuf[P::RPC * P::ROWBUF];
+  __shared__ __align__(16) u64 sbuf[RPC_ * P::ROWBUF];
   const int c0 = threadIdx.x % P::T2;
   const int rr = threadIdx.x / P::T2;
-  const int r = blockIdx.x * P::RPC + rr;
+  const int r = blockIdx.x * RPC_ + rr;
   const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;

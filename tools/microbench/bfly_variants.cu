@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 typedef unsigned long long u64;
@@ -265,6 +266,67 @@ __global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long*
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// V10: hybrid integer/FP64 butterfly.  t = Y w mod q with Y = yh 2^32 + yl:
+//   P = yl w + yh w2 (w2 = w 2^32 mod q), Q = round(P/q - 0.75) from DFMA with
+//   f = w/q, f2 = w2/q (|error| < 2^-18, so Q in {floor(P/q)-1, floor(P/q)}),
+//   r = P - Q q computed exactly mod 2^64 in [0, 2q).
+__device__ __forceinline__ double u32_to_f64(uint32_t x) {
+#ifdef HYB_I2F
+  return __uint2double_rn(x);
+#else
+  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+#endif
+}
+__device__ __forceinline__ void bfly_v10(u64& X, u64& Y, u64 w, u64 w2, double f, double f2, u64 q2, u64 nq) {
+  const uint32_t yl = (uint32_t)Y, yh = (uint32_t)(Y >> 32);
+  const double dl = u32_to_f64(yl), dh = u32_to_f64(yh);
+  const double qf = fma(dh, f2, fma(dl, f, -0.75));
+  const double t = qf + 6755399441055744.0;              // 1.5 * 2^52: low mantissa bits = round(qf)
+  const u64 Qb = (u64)__double_as_longlong(t);
+  const uint32_t Q0 = (uint32_t)Qb, Q1 = (uint32_t)(Qb >> 32) & 1u;
+  u64 r = (u64)yl * w + (u64)yh * w2 + (u64)Q0 * nq + ((u64)(Q1 ? (uint32_t)nq : 0u) << 32);
+  const bool big = (uint32_t)(X >> 32) > (uint32_t)(q2 >> 32);
+  const u64 x = X - (big ? q2 : 0ull);
+  X = x + r;
+  Y = x + q2 - r;
+}
+
+template <int V, int ILP>
+__global__ void k_bfly_h(u64* out, const u64* in, u64 w, u64 w2, double f, double f2, u64 q, long long* cyc) {
+  u64 X[ILP], Y[ILP];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < ILP; ++i) { X[i] = in[(gid * 2 * ILP + 2 * i) % (1 << 20)]; Y[i] = in[(gid * 2 * ILP + 2 * i + 1) % (1 << 20)]; }
+  const u64 q2 = 2 * q, nq = 0ull - q;
+  const u64 wp = (u64)w2;  // unused for V10
+  long long t0 = clock64();
+  for (int it = 0; it < 256; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) {
+      if (V == 10) bfly_v10(X[i], Y[i], w, w2, f, f2, q2, nq);
+      else bfly_v0(X[i], Y[i], w, (u64)f2 /*wp passed via f2 bits below*/, q, q2, nq);
+    }
+  }
+  long long t1 = clock64();
+  for (int i = 0; i < ILP; ++i) { out[gid * 2 * ILP + 2 * i] = X[i]; out[gid * 2 * ILP + 2 * i + 1] = Y[i]; }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  (void)wp;
+}
+
+__global__ void k_dfma(double* out, double a, double b, long long* cyc) {
+  double x[8];
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  long long t0 = clock64();
+  for (int it = 0; it < 1024; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  long long t1 = clock64();
+  double s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 static u64 mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
 
 int main() {
@@ -334,6 +396,55 @@ int main() {
     run(k_bfly<7>, "V7_c_nq_hiword");
     run(k_bfly<8>, "V8_c_approx");
     run(k_bfly<9>, "V9_c_approx_umulhi");
+  }
+  {
+    // hybrid variant
+    const u64 w2 = (u64)(((u128)w << 32) % q);
+    const double f = (double)w / (double)q, f2 = (double)w2 / (double)q;
+    for (int rep = 0; rep < 2; ++rep) {
+      k_bfly_h<10, 4><<<grid, TPB>>>(dout, din, w, w2, f, f2, q, cyc);
+      cudaEventRecord(e0);
+      k_bfly_h<10, 4><<<grid, TPB>>>(dout, din, w, w2, f, f2, q, cyc);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      CK(cudaMemcpy(hc, cyc, grid * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ho, dout, (size_t)nthr * 64, cudaMemcpyDeviceToHost));
+      long long mx = 0; for (int i = 0; i < grid; ++i) if (hc[i] > mx) mx = hc[i];
+      int bad = 0;
+      for (int i = 0; i < 256; ++i) {
+        int t = i / 4, k = i % 4;
+        u64 X = ho[t * 8 + 2 * k] % q, Y = ho[t * 8 + 2 * k + 1] % q;
+        u64 rX = h[t * 8 + 2 * k], rY = h[t * 8 + 2 * k + 1];
+        for (int it = 0; it < 256; ++it) { u64 tt = mulmod(rY, w, q); u64 nx = (rX + tt) % q, ny = (rX + q - tt) % q; rX = nx; rY = ny; }
+        if (X != rX || Y != rY) ++bad;
+      }
+      double bfly_sm = 256.0 * 4 * TPB * CPS;
+      if (rep) printf("{\"variant\":\"V10_hybrid_fp64\",\"bfly_per_clk_per_sm\":%.3f,\"ms\":%.4f,\"bad\":%d}\n", bfly_sm / mx, ms, bad);
+    }
+    // throughput at ILP 8 (no correctness check; 8 pairs per thread, half the CTAs)
+    u64* dout2; CK(cudaMalloc(&dout2, (size_t)nthr * 16 * 8));
+    auto tp = [&](auto kern, const char* name, double fa) {
+      const int g2 = grid / 2;
+      for (int rep = 0; rep < 2; ++rep) {
+        kern<<<g2, TPB>>>(dout2, din, w, w2, f, fa, q, cyc);
+        CK(cudaDeviceSynchronize());
+      }
+      CK(cudaMemcpy(hc, cyc, g2 * 8, cudaMemcpyDeviceToHost));
+      long long mx = 0; for (int i = 0; i < g2; ++i) if (hc[i] > mx) mx = hc[i];
+      printf("{\"variant\":\"%s\",\"bfly_per_clk_per_sm\":%.3f}\n", name, 256.0 * 8 * TPB * (CPS / 2) / mx);
+    };
+    tp(k_bfly_h<10, 8>, "V10_hybrid_ILP8", f2);
+    double wpd; { u64 wpv = wp; memcpy(&wpd, &wpv, 8); }
+    tp(k_bfly_h<0, 8>, "V0_ILP8(wp garbage ok for tput)", 12345.0);
+    double* dd; CK(cudaMalloc(&dd, (size_t)nthr * 8));
+    for (int rep = 0; rep < 2; ++rep) {
+      k_dfma<<<grid, TPB>>>(dd, 1.0000001, 1e-9, cyc);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(hc, cyc, grid * 8, cudaMemcpyDeviceToHost));
+      long long mx = 0; for (int i = 0; i < grid; ++i) if (hc[i] > mx) mx = hc[i];
+      if (rep) printf("{\"kernel\":\"DFMA\",\"ops_per_clk_per_sm\":%.2f}\n", 1024.0 * 8 * TPB * CPS / mx);
+    }
   }
   (void)refX; (void)refY;
   return 0;
