@@ -212,28 +212,53 @@ def cpu_baseline_block(wl, parts, cores, min_seconds=8.0):
                       f"{el:.1f} s wall on {cores} threads; oracle = plain C, exact 128-bit %)"}
 
 
+def reference_sample(parts, frac: int = 8):
+    """A bounded sample of the workload for the CPU reference arm: 1/frac of every
+    part (limbs for the 2^16 part, polynomials for the batched part)."""
+    out = []
+    for (logn, limbs, polys, seed) in parts:
+        if polys >= frac:
+            out.append((logn, limbs, polys // frac, seed))
+        else:
+            out.append((logn, max(1, limbs // frac), polys, seed))
+    return out
+
+
 def bench_reference(args, wl, parts):
+    import oracle as O
+
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     cores = cpu_cores()
-    per = transforms_per_step(parts)
+    sample = reference_sample(parts)
+    per = transforms_per_step(sample)
+    data = []
+    for (logn, limbs, polys, seed) in sample:
+        mods, a, bhat = make_part_inputs(logn, limbs, polys, seed, 0)
+        data.append((mods, [O.min_psi(q, logn) for q in mods], a, bhat))
+
+    def one_step():
+        t0 = time.perf_counter()
+        for mods, psi, a, bhat in data:
+            O.batch(O.OP_POLYMUL_EVAL, a, mods, psi, b=bhat, n_threads=cores)
+        return time.perf_counter() - t0
+
     for _ in range(args.warmup):
-        run_oracle_sample(parts, 0, cores, 0.0)
-    times = []
-    for _ in range(args.steps):
-        reps, el = run_oracle_sample(parts, 0, cores, 0.0)
-        times.append(el)
+        one_step()
+    times = [one_step() for _ in range(args.steps)]
     tot = sum(times)
     value = per * args.steps / tot
+    desc = ", ".join(f"N=2^{lg} x {lm} limbs x {po} polys" for (lg, lm, po, _) in sample)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded SplitMix64 uniform residues)",
-        "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}", "executor": "CPU oracle, all host cores"},
+        "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}", "executor": "CPU oracle (plain C), all host cores",
+                   "sample_per_step": desc},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"full {wl} workload per step on {cores} threads"},
+                         "sample": f"1/8 of {wl} per step ({desc}; {per} limb-transforms) on {cores} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -407,6 +432,83 @@ def bench_ours(args, wl, parts):
         torch.distributed.destroy_process_group()
 
 
+
+# Paper-comparable single-polynomial latency: one 56-bit prime
+# (P:616), one polynomial, forward NTT, N = 2^12 .. 2^16; quoted beside the
+# paper's tab:ntt-mix A100 numbers (context only, other hardware).
+PAPER_A100_M6_US = {12: 7.19, 13: 8.02, 14: 9.55, 15: 11.15, 16: 19.01}
+
+
+def primes_below(bits: int, logn: int, count: int):
+    two_n = 2 << logn
+    k = ((1 << bits) - 1) // two_n
+    out = []
+    while len(out) < count:
+        q = k * two_n + 1
+        if _is_prime(q):
+            out.append(q)
+        k -= 1
+    return out
+
+
+def bench_latency(args):
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    res = {}
+    for logn in range(12, 17):
+        q = primes_below(56, logn, 1)
+        plan = R.Plan(logn, q)
+        a = inputs.residues(0, 1, q, 1 << logn)
+        d = torch.from_numpy(a.view(np.int64)).cuda()
+        o = torch.empty_like(d)
+        for _ in range(20):
+            R.ntt_forward(plan, o, d)
+        torch.cuda.synchronize()
+        # back-to-back (launch overhead overlapped) and isolated (synchronised) latency
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 200
+        e0.record()
+        for _ in range(reps):
+            R.ntt_forward(plan, o, d)
+        e1.record()
+        torch.cuda.synchronize()
+        b2b = e0.elapsed_time(e1) * 1e3 / reps
+        iso = []
+        for _ in range(50):
+            e0.record()
+            R.ntt_forward(plan, o, d)
+            e1.record()
+            torch.cuda.synchronize()
+            iso.append(e0.elapsed_time(e1) * 1e3)
+        # CUDA graph of 100 forward NTTs: GPU-side time per transform without Python launch overhead
+        g = torch.cuda.CUDAGraph()
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_):
+            R.ntt_forward(plan, o, d)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s_):
+                for _ in range(100):
+                    R.ntt_forward(plan, o, d)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph_us = e0.elapsed_time(e1) * 1e3 / 500
+        res[f"2^{logn}"] = {"us_graph": graph_us, "us_back_to_back": b2b, "us_isolated_median": statistics.median(iso),
+                            "paper_A100_M6_us": PAPER_A100_M6_US[logn], "q_bits": q[0].bit_length()}
+    print(json.dumps({"mode": "latency", "metric": "single-polynomial forward NTT latency (us)",
+                      "config": {"primes": "largest q < 2^56 with q = 1 mod 2N (P:616)", "polys": 1},
+                      "results": res}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -416,12 +518,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     wl = args.workload
     parts = WORKLOADS[wl]["parts"]
-    if args.impl == "reference":
+    if args.latency:
+        bench_latency(args)
+    elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:
         bench_ours(args, wl, parts)
