@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -30,7 +31,28 @@ struct rnt_plan_s {
   TW* d_inv = nullptr;
   TW* d_col_fwd = nullptr;  // n >= 11: natural entries [L][2^{n1}]
   TW* d_col_inv = nullptr;
+  // rnt_execute_host pipelining: auxiliary streams, created on first use
+  std::mutex aux_mu;
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  bool is_view = false;     // limb-window view used internally (owns nothing)
 };
+
+// Shallow limb-window view [l0, l0 + nl) of a plan (for batch == 1 chunking).
+static void make_view(const rnt_plan_s* p, uint32_t l0, uint32_t nl, rnt_plan_s* v) {
+  v->logn = p->logn;
+  v->L = nl;
+  v->device = p->device;
+  v->d_lc = p->d_lc + l0;
+  const size_t n = (size_t)1 << p->logn;
+  v->d_fwd = p->d_fwd + l0 * n;
+  v->d_inv = p->d_inv + l0 * n;
+  if (p->d_col_fwd) {
+    const size_t r = (size_t)1 << ((p->logn + 1) / 2);
+    v->d_col_fwd = p->d_col_fwd + l0 * r;
+    v->d_col_inv = p->d_col_inv + l0 * r;
+  }
+  v->is_view = true;
+}
 
 static thread_local int g_last_cuda = 0;
 static std::atomic<uint64_t> g_launches{0};
@@ -407,6 +429,8 @@ rnt_status rnt_plan_destroy(rnt_plan p) {
   cudaFree(p->d_inv);
   cudaFree(p->d_col_fwd);
   cudaFree(p->d_col_inv);
+  for (auto& a : p->aux)
+    if (a) cudaStreamDestroy(a);
   cudaSetDevice(prev);
   delete p;
   return RNT_OK;
@@ -495,15 +519,86 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   if (!out_host || !in_host) return RNT_E_INVALID_ARG;
   rnt_status s = check_data(p, dev_ws, dev_ws, batch);
   if (s != RNT_OK) return s;
-  if ((op == RNT_OP_POLYMUL_EVAL || op == RNT_OP_POLYMUL) && (!b_dev || !aligned16(b_dev) || b_dev == dev_ws))
-    return RNT_E_INVALID_ARG;
+  const bool bop = (op == RNT_OP_POLYMUL_EVAL || op == RNT_OP_POLYMUL);
+  if (bop && (!b_dev || !aligned16(b_dev) || b_dev == dev_ws)) return RNT_E_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t bytes = ((size_t)batch * p->L << p->logn) * 8;
-  RNT_CUDA(cudaMemcpyAsync(dev_ws, in_host, bytes, cudaMemcpyHostToDevice, st));
-  s = run_op(p, (int)op, dev_ws, dev_ws, b_dev, b_broadcast ? 1 : 0, batch, st);
-  if (s != RNT_OK) return s;
-  RNT_CUDA(cudaMemcpyAsync(out_host, dev_ws, bytes, cudaMemcpyDeviceToHost, st));
-  return RNT_OK;
+  const size_t n = (size_t)1 << p->logn;
+  const size_t unit_bytes = n * 8;
+  const size_t total_units = (size_t)batch * p->L;
+  // Chunking: ~8 MiB chunks over polynomials (batch > 1) or limbs (batch == 1),
+  // round-robin over three internal streams so H2D copy, kernels and D2H copy
+  // of successive chunks overlap.  Fork/join with the caller's stream by events.
+  const size_t target = (size_t)8 << 20;
+  size_t per_chunk_units = target / unit_bytes;
+  if (per_chunk_units < 1) per_chunk_units = 1;
+  uint32_t nchunks;
+  if (batch > 1) {
+    size_t polys = per_chunk_units / p->L;
+    if (polys < 1) polys = 1;
+    nchunks = (uint32_t)((batch + polys - 1) / polys);
+  } else {
+    nchunks = (uint32_t)((p->L + per_chunk_units - 1) / per_chunk_units);
+  }
+  if (nchunks <= 1) {
+    RNT_CUDA(cudaMemcpyAsync(dev_ws, in_host, total_units * unit_bytes, cudaMemcpyHostToDevice, st));
+    s = run_op(p, (int)op, dev_ws, dev_ws, b_dev, b_broadcast ? 1 : 0, batch, st);
+    if (s != RNT_OK) return s;
+    RNT_CUDA(cudaMemcpyAsync(out_host, dev_ws, total_units * unit_bytes, cudaMemcpyDeviceToHost, st));
+    return RNT_OK;
+  }
+  {
+    std::lock_guard<std::mutex> g(p->aux_mu);
+    for (auto& a : p->aux)
+      if (!a) RNT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  }
+  cudaEvent_t fork, join[3];
+  RNT_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  RNT_CUDA(cudaEventRecord(fork, st));
+  for (int i = 0; i < 3; ++i) {
+    RNT_CUDA(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    RNT_CUDA(cudaStreamWaitEvent(p->aux[i], fork, 0));
+  }
+  for (uint32_t c = 0; c < nchunks && s == RNT_OK; ++c) {
+    cudaStream_t a = p->aux[c % 3];
+    size_t u0, nu;
+    const uint64_t* bchunk = b_dev;
+    rnt_plan_s view;
+    const rnt_plan_s* pp = p;
+    uint32_t cb = batch;
+    if (batch > 1) {
+      const uint32_t per = (batch + nchunks - 1) / nchunks;
+      const uint32_t b0 = c * per;
+      if (b0 >= batch) break;
+      cb = batch - b0 < per ? batch - b0 : per;
+      u0 = (size_t)b0 * p->L;
+      nu = (size_t)cb * p->L;
+      if (bop && !b_broadcast) bchunk = b_dev + u0 * n;
+    } else {
+      const uint32_t per = (p->L + nchunks - 1) / nchunks;
+      const uint32_t l0 = c * per;
+      if (l0 >= p->L) break;
+      const uint32_t nl = p->L - l0 < per ? p->L - l0 : per;
+      make_view(p, l0, nl, &view);
+      pp = &view;
+      u0 = l0;
+      nu = nl;
+      if (bop) bchunk = b_dev + (size_t)l0 * n;
+    }
+    cudaError_t e = cudaMemcpyAsync(dev_ws + u0 * n, in_host + u0 * n, nu * unit_bytes, cudaMemcpyHostToDevice, a);
+    if (e != cudaSuccess) { s = cuda_fail(e); break; }
+    s = run_op(const_cast<rnt_plan_s*>(pp), (int)op, dev_ws + u0 * n, dev_ws + u0 * n, bchunk,
+               b_broadcast ? 1 : 0, cb, a);
+    if (s != RNT_OK) break;
+    e = cudaMemcpyAsync(out_host + u0 * n, dev_ws + u0 * n, nu * unit_bytes, cudaMemcpyDeviceToHost, a);
+    if (e != cudaSuccess) { s = cuda_fail(e); break; }
+  }
+  for (int i = 0; i < 3; ++i) {
+    cudaEventRecord(join[i], p->aux[i]);
+    cudaStreamWaitEvent(st, join[i], 0);
+    cudaEventDestroy(join[i]);
+  }
+  cudaEventDestroy(fork);
+  return s;
 }
 
 }  // extern "C"

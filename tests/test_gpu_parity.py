@@ -278,3 +278,32 @@ def test_batch_zero_is_noop_and_errors():
     with pytest.raises(R.RntError) as e:
         R.ntt_forward(p, d.view(-1)[1:], d, batch=1)  # misaligned pointer
     assert e.value.code == R.RNT_E_INVALID_ARG
+
+
+@pytest.mark.parametrize("logn,limbs,batch,op", [(10, 1, 4096, "fwd"), (10, 2, 1500, "polymul_eval"),
+                                                 (16, 45, 1, "polymul_eval"), (16, 9, 3, "inv"),
+                                                 (16, 12, 1, "polymul")])
+def test_execute_host_chunked_pipeline(logn, limbs, batch, op):
+    """rnt_execute_host splits large jobs into chunks over 3 internal streams."""
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    a = inputs.residues(12, batch, ps, 1 << logn)
+    hin = torch.from_numpy(a.view(np.int64).copy()).pin_memory()
+    hout = torch.zeros_like(hin).pin_memory()
+    ws = empty_dev(a.shape)
+    if op == "fwd":
+        R.execute_host(p, R.OP_FORWARD, hout, hin, ws)
+        want = O.batch(O.OP_FWD, a, ps, psi, n_threads=8)
+    elif op == "inv":
+        R.execute_host(p, R.OP_INVERSE, hout, hin, ws)
+        want = O.batch(O.OP_INV, a, ps, psi, n_threads=8)
+    else:
+        b = inputs.residues(13, batch, ps, 1 << logn)
+        if op == "polymul_eval":
+            bhat = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+            R.execute_host(p, R.OP_POLYMUL_EVAL, hout, hin, ws, b_dev=to_dev(bhat))
+        else:
+            R.execute_host(p, R.OP_POLYMUL, hout, hin, ws, b_dev=to_dev(b))
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8)
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy().view(np.uint64), want)

@@ -327,6 +327,83 @@ __global__ void k_dfma(double* out, double a, double b, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// V12: exact Shoup, every product a mul.wide/mul.lo with a zero addend (no
+// 64-bit register-pair addends), every sum a 32-bit carry chain.
+__device__ __forceinline__ void bfly_v12(uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1, uint32_t w0,
+                                         uint32_t w1, uint32_t p0, uint32_t p1, uint32_t n0, uint32_t n1,
+                                         uint32_t q20, uint32_t q21) {
+  uint32_t X0, X1, Y0, Y1;
+  asm("{\n\t"
+      ".reg .u32 A, Bl, Bh, Cl, Ch, Dl, Dh, s, Q0, Q1, El, Eh, Fl, Fh, t1, t2, r0, r1, s0, s1, a0, a1;\n\t"
+      ".reg .u64 B, C, D, E, F;\n\t"
+      ".reg .pred big;\n\t"
+      "mul.hi.u32 A, %4, %10;\n\t"
+      "mul.wide.u32 B, %4, %11;\n\t"
+      "mul.wide.u32 C, %5, %10;\n\t"
+      "mul.wide.u32 D, %5, %11;\n\t"
+      "mov.b64 {Bl, Bh}, B;\n\t"
+      "mov.b64 {Cl, Ch}, C;\n\t"
+      "mov.b64 {Dl, Dh}, D;\n\t"
+      "add.cc.u32 s, A, Bl;\n\t"
+      "addc.cc.u32 Q0, Dl, Bh;\n\t"
+      "addc.u32 Q1, Dh, 0;\n\t"
+      "add.cc.u32 s, s, Cl;\n\t"
+      "addc.cc.u32 Q0, Q0, Ch;\n\t"
+      "addc.u32 Q1, Q1, 0;\n\t"
+      "mul.wide.u32 E, %4, %8;\n\t"
+      "mul.wide.u32 F, Q0, %12;\n\t"
+      "mov.b64 {El, Eh}, E;\n\t"
+      "mov.b64 {Fl, Fh}, F;\n\t"
+      "mad.lo.u32 t1, %4, %9, Eh;\n\t"
+      "mad.lo.u32 t1, %5, %8, t1;\n\t"
+      "mad.lo.u32 t2, Q0, %13, Fh;\n\t"
+      "mad.lo.u32 t2, Q1, %12, t2;\n\t"
+      "add.cc.u32 r0, El, Fl;\n\t"
+      "addc.u32 r1, t1, t2;\n\t"
+      "setp.gt.u32 big, %7, %15;\n\t"
+      "selp.u32 s0, %14, 0, big;\n\t"
+      "selp.u32 s1, %15, 0, big;\n\t"
+      "selp.u32 a0, 0, %14, big;\n\t"
+      "selp.u32 a1, 0, %15, big;\n\t"
+      "sub.cc.u32 %0, %6, s0;\n\t"
+      "subc.u32 %1, %7, s1;\n\t"
+      "add.cc.u32 %0, %0, r0;\n\t"
+      "addc.u32 %1, %1, r1;\n\t"
+      "add.cc.u32 %2, %6, a0;\n\t"
+      "addc.u32 %3, %7, a1;\n\t"
+      "sub.cc.u32 %2, %2, r0;\n\t"
+      "subc.u32 %3, %3, r1;\n\t"
+      "}"
+      : "=r"(X0), "=r"(X1), "=r"(Y0), "=r"(Y1)
+      : "r"(y0), "r"(y1), "r"(x0), "r"(x1), "r"(w0), "r"(w1), "r"(p0), "r"(p1), "r"(n0), "r"(n1), "r"(q20),
+        "r"(q21));
+  x0 = X0; x1 = X1; y0 = Y0; y1 = Y1;
+}
+
+__global__ void k_bfly12(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long* cyc) {
+  uint32_t x0[4], x1[4], y0[4], y1[4];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < 4; ++i) {
+    u64 X = in[gid * 8 + 2 * i], Y = in[gid * 8 + 2 * i + 1];
+    x0[i] = (uint32_t)X; x1[i] = (uint32_t)(X >> 32); y0[i] = (uint32_t)Y; y1[i] = (uint32_t)(Y >> 32);
+  }
+  const u64 q2 = 2 * q, nq = 0ull - q;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      bfly_v12(x0[i], x1[i], y0[i], y1[i], (uint32_t)w, (uint32_t)(w >> 32), (uint32_t)wp, (uint32_t)(wp >> 32),
+               (uint32_t)nq, (uint32_t)(nq >> 32), (uint32_t)q2, (uint32_t)(q2 >> 32));
+  }
+  long long t1 = clock64();
+  for (int i = 0; i < 4; ++i) {
+    out[gid * 8 + 2 * i] = ((u64)x1[i] << 32) | x0[i];
+    out[gid * 8 + 2 * i + 1] = ((u64)y1[i] << 32) | y0[i];
+  }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 static u64 mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
 
 int main() {
@@ -396,6 +473,7 @@ int main() {
     run(k_bfly<7>, "V7_c_nq_hiword");
     run(k_bfly<8>, "V8_c_approx");
     run(k_bfly<9>, "V9_c_approx_umulhi");
+    run(k_bfly12, "V12_ptx_noaddend_hiword");
   }
   {
     // hybrid variant
