@@ -45,7 +45,7 @@ static void make_view(const rnt_plan_s* p, uint32_t l0, uint32_t nl, rnt_plan_s*
   v->d_lc = p->d_lc + l0;
   const size_t n = (size_t)1 << p->logn;
   v->d_fwd = p->d_fwd + l0 * n;
-  v->d_inv = p->d_inv + l0 * n;
+  v->d_inv = p->d_inv ? p->d_inv + l0 * n : nullptr;
   if (p->d_col_fwd) {
     const size_t r = (size_t)1 << ((p->logn + 1) / 2);
     v->d_col_fwd = p->d_col_fwd + l0 * r;
@@ -249,8 +249,7 @@ static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, con
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(P::R / RPC_, (unsigned)cnt);
-    k_row<LOGN, MODE, RPC_><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv, p->d_lc, p->L,
-                                                       batch, y0);
+    k_row<LOGN, MODE, RPC_><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -378,7 +377,9 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
     lc[l].ninvR = TW{h.ninvR.w, h.ninvR.wp};
     lc[l].ninvR_w1 = TW{h.ninvR_w1.w, h.ninvR_w1.wp};
   }
-  std::vector<HostTW> nat(n), lay((size_t)n_limbs * n), layi((size_t)n_limbs * n);
+  // large N: the inverse row stages mirror the forward row table (ntt_large.cuh),
+  // so only the small column table is kept per direction.
+  std::vector<HostTW> nat(n), lay((size_t)n_limbs * n), layi(large ? 0 : (size_t)n_limbs * n);
   std::vector<HostTW> col, coli;
   if (large) {
     col.resize((size_t)n_limbs << n1);
@@ -387,11 +388,11 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   for (uint32_t l = 0; l < n_limbs; ++l) {
     for (int dir = 0; dir < 2; ++dir) {
       plan_powers(limbs[l], log2n, dir == 1, n, nat.data());
-      HostTW* dst = (dir ? layi.data() : lay.data()) + (size_t)l * n;
       if (large) {
-        plan_row_layout(nat.data(), log2n, dst);
+        if (dir == 0) plan_row_layout(nat.data(), log2n, lay.data() + (size_t)l * n);
         std::memcpy((dir ? coli.data() : col.data()) + ((size_t)l << n1), nat.data(), sizeof(HostTW) << n1);
       } else {
+        HostTW* dst = (dir ? layi.data() : lay.data()) + (size_t)l * n;
         std::memcpy(dst, nat.data(), sizeof(HostTW) * n);  // natural order (ntt_small.cuh)
       }
     }
@@ -404,10 +405,11 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   cudaError_t e;
   if ((e = cudaMalloc(&p->d_lc, sizeof(LimbC) * n_limbs)) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&p->d_fwd, sizeof(TW) * lay.size())) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc(&p->d_inv, sizeof(TW) * layi.size())) != cudaSuccess) return fail(e);
+  if (!large && (e = cudaMalloc(&p->d_inv, sizeof(TW) * layi.size())) != cudaSuccess) return fail(e);
   if ((e = cudaMemcpy(p->d_lc, lc.data(), sizeof(LimbC) * n_limbs, cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
   if ((e = cudaMemcpy(p->d_fwd, lay.data(), sizeof(TW) * lay.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
-  if ((e = cudaMemcpy(p->d_inv, layi.data(), sizeof(TW) * layi.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  if (!large && (e = cudaMemcpy(p->d_inv, layi.data(), sizeof(TW) * layi.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e);
   if (large) {
     if ((e = cudaMalloc(&p->d_col_fwd, sizeof(TW) * col.size())) != cudaSuccess) return fail(e);
     if ((e = cudaMalloc(&p->d_col_inv, sizeof(TW) * coli.size())) != cudaSuccess) return fail(e);

@@ -81,6 +81,17 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
   Y = shoup_lazy(d, t, q);      // [0, 2q)
 }
 
+// GS butterfly with a negated twiddle: (X, Y) -> (X + Y, (Y - X) w).  With
+// w = psi^{brv(k')} of the mirrored index k' = 3 2^s - 1 - k this equals the GS
+// butterfly with psi^{-brv(k)} = -psi^{brv(k')}, so inverse row stages can read
+// the forward twiddle table (ntt_large.cuh).
+__device__ __forceinline__ void gs_bfly_neg(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  u64 s = csub(X + Y, q2);      // [0, 2q)
+  u64 d = Y + q2 - X;           // (0, 4q)
+  X = s;
+  Y = shoup_lazy(d, t, q);      // [0, 2q)
+}
+
 // Last GS stage (t = N/2, twiddle psi^{-brv(1)}) with the N^{-1} scaling of
 // S:167 folded in: X' = (X + Y) N^{-1}, Y' = (X - Y) psi^{-brv(1)} N^{-1}.
 __device__ __forceinline__ void gs_bfly_last(u64& X, u64& Y, TW s0, TW s1, u64 q, u64 q2) {

@@ -155,7 +155,7 @@ k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
 }
 
 // ============================== pass 2 (rows) =================================
-// Row twiddle table (per limb, per row r, 2^{n2} entries): stage v (global
+// Row twiddle table (forward only; per limb, per row r, 2^{n2} entries): stage v (global
 // stage n1 + v) occupies [2^v - 1, 2^{v+1} - 1); for v < 4 entry k holds
 // w[2^{n1+v} + r 2^v + k]; for v >= 4 entry m*T2 + c1 holds
 // w[2^{n1+v} + r 2^v + c1 2^{v+4-n2} + m] (lane-major: coalesced loads).
@@ -189,31 +189,35 @@ __device__ __forceinline__ void row_fwd_B(u64 (&x)[kEl], const TW* Tr, int c1, u
   });
 }
 
+// Inverse row stages read the FORWARD row table of the mirrored row R-1-r,
+// block-reversed (psi^{-brv(k)} = -psi^{brv(3 2^s - 1 - k)}), with the
+// negated-twiddle GS butterfly: no inverse row table exists.
 template <int LOGN>
-__device__ __forceinline__ void row_inv_B(u64 (&x)[kEl], const TW* Tr, int c1, u64 q, u64 q2) {
+__device__ __forceinline__ void row_inv_B(u64 (&x)[kEl], const TW* Tm, int c1, u64 q, u64 q2) {
   using P = TwoPass<LOGN>;
   sfor<0, P::n2 - 4>([&](auto I_) {
     constexpr int v = P::n2 - 1 - decltype(I_)::value;
     constexpr int t = P::Cn >> (v + 1);
+    constexpr int per = kEl / (2 * t);
 #pragma unroll
-    for (int m = 0; m < kEl / (2 * t); ++m) {
-      TW w = ldg_tw(Tr + (1 << v) - 1 + m * P::T2 + c1);
+    for (int m = 0; m < per; ++m) {
+      TW w = ldg_tw(Tm + (1 << v) - 1 + (per - 1 - m) * P::T2 + (P::T2 - 1 - c1));
 #pragma unroll
-      for (int k = 0; k < t; ++k) gs_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+      for (int k = 0; k < t; ++k) gs_bfly_neg(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
     }
   });
 }
 
 template <int LOGN>
-__device__ __forceinline__ void row_inv_A(u64 (&x)[kEl], const TW* Tr, u64 q, u64 q2) {
+__device__ __forceinline__ void row_inv_A(u64 (&x)[kEl], const TW* Tm, u64 q, u64 q2) {
   sfor<0, 4>([&](auto I_) {
     constexpr int v = 3 - decltype(I_)::value;
     constexpr int half = kEl >> (v + 1);
 #pragma unroll
     for (int blk = 0; blk < (1 << v); ++blk) {
-      TW w = ldg_tw(Tr + (1 << v) - 1 + blk);
+      TW w = ldg_tw(Tm + (1 << v) - 1 + ((1 << v) - 1 - blk));
 #pragma unroll
-      for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      for (int k = 0; k < half; ++k) gs_bfly_neg(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
     }
   });
 }
@@ -247,13 +251,21 @@ __device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
 template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC>
 __global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2)
 k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
-      const TW* __restrict__ tw_row_fwd, const TW* __restrict__ tw_row_inv,
-      const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+      const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
   __shared__ __align__(16) u64 sbuf[RPC_ * P::ROWBUF];
   const int c0 = threadIdx.x % P::T2;
   const int rr = threadIdx.x / P::T2;
-  const int r = blockIdx.x * RPC_ + rr;
+  // With 16 threads per row a warp holds two rows: make them r and R-1-r, so
+  // the inverse stages of each row read (from L1) the forward twiddles its
+  // partner half-warp just loaded.
+  int r;
+  if constexpr (P::T2 == 16 && RPC_ % 2 == 0) {
+    const int pi = blockIdx.x * (RPC_ / 2) + (rr >> 1);
+    r = (rr & 1) ? (P::R - 1 - pi) : pi;
+  } else {
+    r = blockIdx.x * RPC_ + rr;
+  }
   const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
@@ -261,14 +273,15 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   u64* rb = sbuf + rr * P::ROWBUF;
   const size_t rowoff = u * (size_t)(P::R * P::Cn) + (size_t)r * P::Cn;
   const size_t troff = ((size_t)l * P::R + r) * P::Cn;
+  const TW* Tm = tw_row_fwd + ((size_t)l * P::R + (P::R - 1 - r)) * P::Cn;   // mirrored row
   u64 x[kEl];
 #pragma unroll
   for (int i = 0; i < kEl; ++i) x[i] = in[rowoff + c0 + P::T2 * i];
   if (MODE == 1) {
     row_A_to_B<LOGN>(x, rb, c0);
-    row_inv_B<LOGN>(x, tw_row_inv + troff, c0, q, q2);
+    row_inv_B<LOGN>(x, Tm, c0, q, q2);
     row_B_to_A<LOGN>(x, rb, c0);
-    row_inv_A<LOGN>(x, tw_row_inv + troff, q, q2);
+    row_inv_A<LOGN>(x, Tm, q, q2);
   } else {
     const TW* Tf = tw_row_fwd + troff;
     row_fwd_A<LOGN>(x, Tf, q, q2);
@@ -290,10 +303,9 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
 #pragma unroll
       for (int i = 0; i < kEl; ++i) x[i] = mont_mul(x[i], rb[row_swz<LOGN>(kEl * c0 + i)], q, qinv);
       __syncwarp();
-      const TW* Ti = tw_row_inv + troff;
-      row_inv_B<LOGN>(x, Ti, c0, q, q2);
+      row_inv_B<LOGN>(x, Tm, c0, q, q2);
       row_B_to_A<LOGN>(x, rb, c0);
-      row_inv_A<LOGN>(x, Ti, q, q2);
+      row_inv_A<LOGN>(x, Tm, q, q2);
     }
   }
 #pragma unroll
