@@ -108,13 +108,13 @@ static int num_sms() {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE, int W, int MINB, bool SYNC>
+template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
   static bool attr_set = false;  // benign race: idempotent attribute call
   const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
   if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE, W, MINB, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE, W, MINB, SYNC, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     attr_set = true;
   }
@@ -123,7 +123,7 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    k_warp<LOGN, MODE, W, MINB, SYNC><<<grid, W * 32, smem, st>>>(
+    k_warp<LOGN, MODE, W, MINB, SYNC, KM><<<grid, W * 32, smem, st>>>(
         out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
         p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
@@ -182,11 +182,19 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
       case 6: return launch_warp_tma<LOGN, MODE, 2>(p, out, in, bop, bcast, batch, st);
       case 1: return launch_warp_v<LOGN, MODE, 4, 4, false>(p, out, in, bop, bcast, batch, st);
       case 7: return launch_warp_v<LOGN, MODE, kTeamWarps, 1, false>(p, out, in, bop, bcast, batch, st);
+      case 8: return launch_warp_v<LOGN, MODE, 2, 8, false, 4>(p, out, in, bop, bcast, batch, st);
+      case 9: return launch_warp_v<LOGN, MODE, 4, 4, false, 3>(p, out, in, bop, bcast, batch, st);
+      case 10: return launch_warp_v<LOGN, MODE, 2, 8, false, 5>(p, out, in, bop, bcast, batch, st);
+      case 11: return launch_warp_v<LOGN, MODE, 2, 16, false, 3>(p, out, in, bop, bcast, batch, st);
+      case 12: return launch_warp_v<LOGN, MODE, 4, 6, false, 3>(p, out, in, bop, bcast, batch, st);
+      case 13: return launch_warp_v<LOGN, MODE, 2, 16, false, 2>(p, out, in, bop, bcast, batch, st);
+      case 14: return launch_warp_v<LOGN, MODE, 1, 24, false, 3>(p, out, in, bop, bcast, batch, st);
       default: break;
     }
   }
-  // default: 2 warps per CTA, <= 128 registers (16 warps/SM) -- fastest measured
-  return launch_warp_v<LOGN, MODE, 2, 8, false>(p, out, in, bop, bcast, batch, st);
+  // default: radix-8 passes (N=2^10: 3+3+3+1), 2 warps per CTA, <= 85 registers
+  // (24 warps/SM) -- fastest measured (profiles/r01/README.md)
+  return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 
 template <int MODE>

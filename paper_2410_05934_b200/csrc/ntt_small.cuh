@@ -268,77 +268,58 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
 }
 
 // ---- full transforms on one warp buffer ---------------------------------------
-template <int LOGN, int DST, bool SYNC = false>
+// Pass schedule: stages grouped into passes of KM (the last takes the
+// remainder), e.g. N = 2^10: KM = 4 -> 4 + 4 + 2, KM = 3 -> 3 + 3 + 3 + 1.
+template <int LOGN, int KM>
+struct Passes {
+  static constexpr int NP = (LOGN + KM - 1) / KM;
+  __host__ __device__ static constexpr int k(int p) { return p < NP - 1 ? KM : LOGN - KM * (NP - 1); }
+  __host__ __device__ static constexpr int s(int p) { return p * KM; }
+};
+
+template <int LOGN, int KM, int DST, bool SYNC = false>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
-  using C = WarpCfg<LOGN>;
-  if constexpr (C::NPASS == 1) {
-    fwd_pass<LOGN, 0, C::K0, kFromGlobal, DST>(buf, src, dst, lane, T, q, q2);
+  using PS = Passes<LOGN, KM>;
+  sfor<0, PS::NP>([&](auto P_) {
+    constexpr int p = decltype(P_)::value;
+    constexpr int SRC = p == 0 ? kFromGlobal : kFromBuf;
+    constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
+    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
-  } else if constexpr (C::NPASS == 2) {
-    fwd_pass<LOGN, 0, C::K0, kFromGlobal, kToBuf>(buf, src, dst, lane, T, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    fwd_pass<LOGN, C::K0, C::K1, kFromBuf, DST>(buf, src, dst, lane, T, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  } else {
-    fwd_pass<LOGN, 0, C::K0, kFromGlobal, kToBuf>(buf, src, dst, lane, T, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    fwd_pass<LOGN, C::K0, C::K1, kFromBuf, kToBuf>(buf, src, dst, lane, T, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    fwd_pass<LOGN, C::K0 + C::K1, C::K2, kFromBuf, DST>(buf, src, dst, lane, T, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  }
+  });
 }
 
-template <int LOGN, bool SYNC = false>
+template <int LOGN, int KM, bool SYNC = false>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
-  using C = WarpCfg<LOGN>;
-  if constexpr (C::NPASS == 1) {
-    inv_pass<LOGN, 0, C::K0, kFromGlobal, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
+  using PS = Passes<LOGN, KM>;
+  sfor<0, PS::NP>([&](auto I_) {
+    constexpr int i = decltype(I_)::value;
+    constexpr int p = PS::NP - 1 - i;
+    constexpr int SRC = i == 0 ? kFromGlobal : kFromBuf;
+    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, p == 0>(buf, src, dst, lane, T, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
-  } else if constexpr (C::NPASS == 2) {
-    inv_pass<LOGN, C::K0, C::K1, kFromGlobal, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  } else {
-    inv_pass<LOGN, C::K0 + C::K1, C::K2, kFromGlobal, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, C::K0, C::K1, kFromBuf, false, false>(buf, src, dst, lane, T, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, src, dst, lane, T, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  }
+  });
 }
 
-template <int LOGN, int BSRC, bool SYNC = false>
+template <int LOGN, int KM, int BSRC, bool SYNC = false>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
-  using C = WarpCfg<LOGN>;
-  if constexpr (C::NPASS == 1) {
-    turn_pass<LOGN, 0, C::K0, kFromGlobal, true, BSRC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
+  using PS = Passes<LOGN, KM>;
+  constexpr int NP = PS::NP;
+  sfor<0, NP - 1>([&](auto P_) {
+    constexpr int p = decltype(P_)::value;
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf>(buf, src, dst, lane, Tf, q, q2);
     if constexpr (SYNC) __syncthreads();
-  } else if constexpr (C::NPASS == 2) {
-    fwd_pass<LOGN, 0, C::K0, kFromGlobal, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+  });
+  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC>(
+      buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
+  if constexpr (SYNC) __syncthreads();
+  sfor<0, NP - 1>([&](auto I_) {
+    constexpr int p = NP - 2 - decltype(I_)::value;
+    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(buf, src, dst, lane, Ti, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
-    turn_pass<LOGN, C::K0, C::K1, kFromBuf, false, BSRC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2,
-                                                          qinv);
-                                                          if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  } else {
-    fwd_pass<LOGN, 0, C::K0, kFromGlobal, kToBuf>(buf, src, dst, lane, Tf, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    fwd_pass<LOGN, C::K0, C::K1, kFromBuf, kToBuf>(buf, src, dst, lane, Tf, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    turn_pass<LOGN, C::K0 + C::K1, C::K2, kFromBuf, false, BSRC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1,
-                                                                  q, q2, qinv);
-                                                                  if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, C::K0, C::K1, kFromBuf, false, false>(buf, src, dst, lane, Ti, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-    inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, src, dst, lane, Ti, s0, s1, q, q2);
-    if constexpr (SYNC) __syncthreads();
-  }
+  });
 }
 
 // ---- kernel --------------------------------------------------------------------
@@ -346,7 +327,7 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
-template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false>
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4>
 __global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
@@ -367,19 +348,19 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Tf = tw_fwd + (size_t)l * N;
   const TW* Ti = tw_inv + (size_t)l * N;
   if constexpr (MODE == 0) {
-    warp_forward<LOGN, kToGlobal, SYNC>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<LOGN, KM, kToGlobal, SYNC>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<LOGN, SYNC>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+    warp_inverse<LOGN, KM, SYNC>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
   } else {
     const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
     const u64 qinv = lc[l].qinv;
     if constexpr (MODE == 3) {
       u64* bbuf = buf + kWarpBuf;
       // canonical NTT(b) parked in the second warp buffer
-      warp_forward<LOGN, kToBufCanon, SYNC>(bbuf, bview, bview, lane, Tf, q, q2);
-      warp_polymul<LOGN, kFromBuf, SYNC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+      warp_forward<LOGN, KM, kToBufCanon, SYNC>(bbuf, bview, bview, lane, Tf, q, q2);
+      warp_polymul<LOGN, KM, kFromBuf, SYNC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     } else {
-      warp_polymul<LOGN, kFromGlobal, SYNC>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
+      warp_polymul<LOGN, KM, kFromGlobal, SYNC>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
                                 qinv);
     }
   }
