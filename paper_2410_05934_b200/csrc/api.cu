@@ -31,6 +31,7 @@ struct rnt_plan_s {
   TW* d_inv = nullptr;
   TW* d_col_fwd = nullptr;  // n >= 11: natural entries [L][2^{n1}]
   TW* d_col_inv = nullptr;
+  TW* d_rowtw = nullptr;    // n >= 11: natural per-row forward table [L][2^{n1}][2^{n2}] (k_rows)
   // rnt_execute_host pipelining: auxiliary streams, created on first use
   std::mutex aux_mu;
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
@@ -50,6 +51,7 @@ static void make_view(const rnt_plan_s* p, uint32_t l0, uint32_t nl, rnt_plan_s*
     const size_t r = (size_t)1 << ((p->logn + 1) / 2);
     v->d_col_fwd = p->d_col_fwd + l0 * r;
     v->d_col_inv = p->d_col_inv + l0 * r;
+    v->d_rowtw = p->d_rowtw + l0 * n;
   }
   v->is_view = true;
 }
@@ -265,8 +267,32 @@ static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, con
 }
 
 template <int LOGN, int MODE>
+static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                   uint32_t batch, cudaStream_t st) {
+  using P = TwoPass<LOGN>;
+  static bool attr_set = false;  // benign race: idempotent attribute call
+  const size_t smem = (size_t)kRowWarps * kWarpBuf * 8;
+  if (!attr_set) {
+    RNT_CUDA(cudaFuncSetAttribute(k_rows<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  constexpr int rows_per_cta = kRowWarps * (kWarpElems / P::Cn);
+  const unsigned gx = (unsigned)((P::R + rows_per_cta - 1) / rows_per_cta);
+  const uint64_t units = (uint64_t)batch * p->L;
+  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
+    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
+    dim3 g(gx, (unsigned)cnt);
+    k_rows<LOGN, MODE><<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  return RNT_OK;
+}
+
+template <int LOGN, int MODE>
 static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                              uint32_t batch, cudaStream_t st) {
+  if (large_variant() & 4) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
   constexpr int R4 = TwoPass<LOGN>::RPC / 4 > 0 ? TwoPass<LOGN>::RPC / 4 : 1;
   if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4>(p, out, in, bop, bcast, batch, st);
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
@@ -388,8 +414,9 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   // large N: the inverse row stages mirror the forward row table (ntt_large.cuh),
   // so only the small column table is kept per direction.
   std::vector<HostTW> nat(n), lay((size_t)n_limbs * n), layi(large ? 0 : (size_t)n_limbs * n);
-  std::vector<HostTW> col, coli;
+  std::vector<HostTW> col, coli, rowtw;
   if (large) {
+    rowtw.resize((size_t)n_limbs * n);
     col.resize((size_t)n_limbs << n1);
     coli.resize((size_t)n_limbs << n1);
   }
@@ -397,7 +424,10 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
     for (int dir = 0; dir < 2; ++dir) {
       plan_powers(limbs[l], log2n, dir == 1, n, nat.data());
       if (large) {
-        if (dir == 0) plan_row_layout(nat.data(), log2n, lay.data() + (size_t)l * n);
+        if (dir == 0) {
+          plan_row_layout(nat.data(), log2n, lay.data() + (size_t)l * n);
+          plan_row_natural(nat.data(), log2n, rowtw.data() + (size_t)l * n);
+        }
         std::memcpy((dir ? coli.data() : col.data()) + ((size_t)l << n1), nat.data(), sizeof(HostTW) << n1);
       } else {
         HostTW* dst = (dir ? layi.data() : lay.data()) + (size_t)l * n;
@@ -423,6 +453,8 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
     if ((e = cudaMalloc(&p->d_col_inv, sizeof(TW) * coli.size())) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpy(p->d_col_fwd, col.data(), sizeof(TW) * col.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpy(p->d_col_inv, coli.data(), sizeof(TW) * coli.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&p->d_rowtw, sizeof(TW) * rowtw.size())) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpy(p->d_rowtw, rowtw.data(), sizeof(TW) * rowtw.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
   }
   cudaSetDevice(prev);
   *out = p;
@@ -439,6 +471,7 @@ rnt_status rnt_plan_destroy(rnt_plan p) {
   cudaFree(p->d_inv);
   cudaFree(p->d_col_fwd);
   cudaFree(p->d_col_inv);
+  cudaFree(p->d_rowtw);
   for (auto& a : p->aux)
     if (a) cudaStreamDestroy(a);
   cudaSetDevice(prev);

@@ -312,4 +312,52 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   for (int i = 0; i < kEl; ++i) out[rowoff + c0 + P::T2 * i] = x[i];
 }
 
+// ============================ pass 2, warp engine =============================
+// Rows through the warp engine of ntt_small.cuh: a warp owns 1024 / 2^{n2}
+// consecutive rows of one limb in a padded shared buffer and runs the row
+// stages as radix-8 passes (n2 = 8: 3 + 3 + 2).  Row r uses its own twiddle
+// table T_r[2^s + i] = w[2^{n1+s} + r 2^s + i] (natural per-row layout,
+// stride 2^{n2}); the inverse stages read the mirrored row R-1-r
+// (MIRROR, negated-twiddle GS butterfly) and never apply N^{-1}.
+// MODE 0: forward rows, 1: inverse rows, 2: forward rows -> (.) b_hat -> inverse rows.
+constexpr int kRowWarps = 2;
+constexpr int kRowKM = 3;
+
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(kRowWarps * 32, 12)
+k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
+       const TW* __restrict__ tw_rows, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+  using P = TwoPass<LOGN>;
+  constexpr int n2 = P::n2;
+  constexpr int N2 = P::Cn;
+  constexpr int RPW = kWarpElems / N2;   // rows per warp
+  extern __shared__ __align__(16) u64 smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t y = y0 + blockIdx.y;
+  const uint32_t l = (uint32_t)(y / B);
+  const uint64_t u = (y % B) * L + l;
+  const int r0 = (blockIdx.x * kRowWarps + warp) * RPW;
+  if (r0 >= P::R) return;
+  u64* buf = smem + (size_t)warp * kWarpBuf;
+  const u64 q = lc[l].q, q2 = lc[l].q2;
+  const size_t base = u * (size_t)(P::R * P::Cn);
+  const GView src{in + base, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
+  const GView dst{out + base, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
+  const TW* Tr = tw_rows + (size_t)l * P::R * N2;
+  const TW* Tf = Tr + (size_t)r0 * N2;                  // row r0 (+ p * N2)
+  const TW* Tm = Tr + (size_t)(P::R - 1 - r0) * N2;     // mirrored row R-1-r0 (- p * N2)
+  const TW none{0, 0};
+  if constexpr (MODE == 0) {
+    warp_forward<n2, kRowKM, kToGlobal, false, N2>(buf, src, dst, lane, Tf, q, q2);
+  } else if constexpr (MODE == 1) {
+    warp_inverse<n2, kRowKM, false, false, N2, true>(buf, src, dst, lane, Tm, none, none, q, q2);
+  } else {
+    const size_t boff = b_bcast ? (size_t)l * P::R * P::Cn : base;
+    const GView bview{bop + boff, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
+    warp_polymul<n2, kRowKM, kFromGlobal, false, false, N2, true>(buf, src, dst, bview, nullptr, lane, Tf, Tm, none,
+                                                                  none, q, q2, lc[l].qinv);
+  }
+}
+
 }  // namespace rnt

@@ -91,7 +91,7 @@ __device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, 
 
 // K GS stages (reverse order).  If LAST (S == 0), local stage 0 is the final
 // stage of the inverse and carries the N^{-1} (or N^{-1} R) factor.
-template <int S, int K, bool LAST>
+template <int S, int K, bool LAST, bool MIRROR = false>
 __device__ __forceinline__ void gs_group(u64 (&x)[1 << K], const TW* T, int hi, TW s0, TW s1, u64 q, u64 q2) {
   sfor<0, K>([&](auto I_) {
     constexpr int v = K - 1 - decltype(I_)::value;
@@ -102,9 +102,17 @@ __device__ __forceinline__ void gs_group(u64 (&x)[1 << K], const TW* T, int hi, 
     } else {
 #pragma unroll
       for (int blk = 0; blk < (1 << v); ++blk) {
-        TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
+        if constexpr (MIRROR) {
+          // psi^{-brv(k)} = -psi^{brv(3 2^s - 1 - k)}: read the mirrored forward
+          // entry and use the negated-twiddle butterfly (ntt_large.cuh rows)
+          TW w = ldg_tw(T + (2 << (S + v)) - 1 - (hi * (1 << v) + blk));
 #pragma unroll
-        for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+          for (int k = 0; k < half; ++k) gs_bfly_neg(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+        } else {
+          TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
+#pragma unroll
+          for (int k = 0; k < half; ++k) gs_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+        }
       }
     }
   });
@@ -131,7 +139,9 @@ constexpr int kToGlobal = 1;   // canonical values to global memory
 constexpr int kToBufCanon = 2; // canonical values into the warp buffer
 
 // ---- one forward pass (CT) over the warp buffer -----------------------------
-template <int LOGN, int S, int K, int SRC, int DST>
+// TWS: twiddle-table stride per polynomial of the warp (0: all polynomials
+// share T; 2^{n2}: row r + p of a 2^16 limb uses row table r + p).
+template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0>
 __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2,
                                          const u64* raw = nullptr) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -154,7 +164,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
-    ct_group<S, K>(x, T, g.hi, q, q2);
+    ct_group<S, K>(x, T + g.poly * TWS, g.hi, q, q2);
     if constexpr (DST == kToGlobal) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -170,7 +180,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
   __syncwarp();
 }
 
-template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST>
+template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST, int TWS = 0, bool MIRROR = false>
 __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                          u64 q, u64 q2, const u64* raw = nullptr) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -193,7 +203,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
-    gs_group<S, K, LAST>(x, T, g.hi, s0, s1, q, q2);
+    gs_group<S, K, LAST, MIRROR>(x, MIRROR ? T - g.poly * TWS : T + g.poly * TWS, g.hi, s0, s1, q, q2);
     if constexpr (DST_GLOBAL) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -211,7 +221,8 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 // Fused turn-around pass of the polymul: last CT pass -> (.) b_hat -> first
 // GS pass, all in registers.  b_hat comes from global memory (bview) or from
 // a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf), or a TMA-staged raw buffer (kFromRaw).
-template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC>
+template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC, bool SCALE = true, int TWS = 0,
+          bool MIRROR = false>
 __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                           const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv,
                                           const u64* raw = nullptr, const u64* braw = nullptr) {
@@ -249,10 +260,10 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) bv[i] = live ? __ldg(b + i * Geo::LO) : 0ull;
     }
-    ct_group<S, K>(x, Tf, g.hi, q, q2);
+    ct_group<S, K>(x, Tf + g.poly * TWS, g.hi, q, q2);
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bv[i], q, qinv);
-    gs_group<S, K, S == 0>(x, Ti, g.hi, s0, s1, q, q2);
+    gs_group<S, K, SCALE && S == 0, MIRROR>(x, MIRROR ? Ti - g.poly * TWS : Ti + g.poly * TWS, g.hi, s0, s1, q, q2);
     if constexpr (DST_GLOBAL) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -277,19 +288,19 @@ struct Passes {
   __host__ __device__ static constexpr int s(int p) { return p * KM; }
 };
 
-template <int LOGN, int KM, int DST, bool SYNC = false>
+template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
     constexpr int SRC = p == 0 ? kFromGlobal : kFromBuf;
     constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
 
-template <int LOGN, int KM, bool SYNC = false>
+template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
@@ -297,27 +308,29 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
     constexpr int i = decltype(I_)::value;
     constexpr int p = PS::NP - 1 - i;
     constexpr int SRC = i == 0 ? kFromGlobal : kFromBuf;
-    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, p == 0>(buf, src, dst, lane, T, s0, s1, q, q2);
+    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR>(buf, src, dst, lane, T, s0, s1, q,
+                                                                                  q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
 
-template <int LOGN, int KM, int BSRC, bool SYNC = false>
+template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using PS = Passes<LOGN, KM>;
   constexpr int NP = PS::NP;
   sfor<0, NP - 1>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf>(buf, src, dst, lane, Tf, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS>(buf, src, dst, lane, Tf, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
-  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC>(
+  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR>(
       buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
   if constexpr (SYNC) __syncthreads();
   sfor<0, NP - 1>([&](auto I_) {
     constexpr int p = NP - 2 - decltype(I_)::value;
-    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(buf, src, dst, lane, Ti, s0, s1, q, q2);
+    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, SCALE && p == 0, TWS, MIRROR>(buf, src, dst, lane, Ti, s0, s1,
+                                                                                       q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }

@@ -160,3 +160,14 @@ void plan_row_layout(const HostTW* nat, uint32_t logn, HostTW* out) {
 }
 
 }  // namespace rnt
+
+namespace rnt {
+void plan_row_natural(const HostTW* nat, uint32_t logn, HostTW* out) {
+  const uint32_t n1 = (logn + 1) / 2, n2 = logn / 2, R = 1u << n1, Cn = 1u << n2;
+  std::memset(out, 0, sizeof(HostTW) * (size_t)R * Cn);
+  for (uint32_t r = 0; r < R; ++r)
+    for (uint32_t v = 0; v < n2; ++v)
+      for (uint32_t j = 0; j < (1u << v); ++j)
+        out[(size_t)r * Cn + (1u << v) + j] = nat[(1u << (n1 + v)) + r * (1u << v) + j];
+}
+}  // namespace rnt

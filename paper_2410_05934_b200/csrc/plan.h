@@ -40,5 +40,8 @@ void plan_powers(const HostLimb& lm, uint32_t logn, bool inverse, uint32_t count
 //   column layout = first 2^{n1} natural entries.
 void plan_team_layout(const HostTW* natural, uint32_t logn, HostTW* out);
 void plan_row_layout(const HostTW* natural, uint32_t logn, HostTW* out);
+// Natural per-row layout for the warp-engine row kernel (k_rows):
+// out[r 2^{n2} + 2^v + j] = natural[2^{n1+v} + r 2^v + j].
+void plan_row_natural(const HostTW* natural, uint32_t logn, HostTW* out);
 
 }  // namespace rnt

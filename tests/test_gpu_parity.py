@@ -307,3 +307,39 @@ def test_execute_host_chunked_pipeline(logn, limbs, batch, op):
         want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8)
     torch.cuda.synchronize()
     assert np.array_equal(hout.numpy().view(np.uint64), want)
+
+
+VARIANT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import inputs, oracle as O, paper_2410_05934_b200 as R
+from helpers import params, to_dev, from_dev, empty_dev
+ok = True
+for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3)):
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    a = inputs.residues(3, batch, ps, 1 << logn); b = inputs.residues(4, batch, ps, 1 << logn)
+    bh = O.batch(O.OP_FWD, b, ps, psi)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a)); ok &= np.array_equal(from_dev(d), bh * 0 + O.batch(O.OP_FWD, a, ps, psi))
+    R.ntt_inverse(p, d, to_dev(bh)); ok &= np.array_equal(from_dev(d), b)
+    R.polymul(p, d, to_dev(a), to_dev(bh), b_is_eval=True)
+    ok &= np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bh))
+print("VARIANT_OK" if ok else "VARIANT_BAD")
+"""
+
+
+@pytest.mark.parametrize("env", [{"RNT_SMALL_VARIANT": str(v)} for v in (1, 4, 5, 6, 7, 8, 11, 13)] +
+                         [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)])
+def test_kernel_variants(env):
+    """Every shipped launch variant (selected by env knobs, read once per process)
+    is bit-exact against the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = VARIANT_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
+    assert "VARIANT_OK" in r.stdout, r.stdout + r.stderr
