@@ -65,6 +65,7 @@ def _load():
                 "or_naive_intt_at": (u64, [_u64p, u32, u64, u64, u32]),
                 "or_schoolbook_at": (u64, [_u64p, _u64p, u32, u64, u32]),
                 "or_schoolbook": (None, [_u64p, _u64p, _u64p, u32, u64]),
+                "or_automorph": (None, [_u64p, _u64p, u32, u64, u64]),
                 "or_batch": (i32, [i32, _u64p, _u64p, i32, u32, u32, u32, _u64p, _u64p, i32]),
             }
             for name, (res, args) in sig.items():
@@ -194,6 +195,14 @@ def schoolbook(a, b, q: int) -> np.ndarray:
 def schoolbook_at(a, b, q: int, k: int) -> int:
     a, b = _vec(a), _vec(b)
     return int(_load().or_schoolbook_at(_p(a), _p(b), int(a.size).bit_length() - 1, q, k))
+
+
+def automorph(a, q: int, g: int) -> np.ndarray:
+    """sigma_g(a)(x) = a(x^g) mod (x^N + 1), g odd (Automorph)."""
+    a = _vec(a)
+    out = np.zeros_like(a)
+    _load().or_automorph(_p(out), _p(a), int(a.size).bit_length() - 1, q, g)
+    return out
 
 
 # -------------------------------------------------------------------- batch

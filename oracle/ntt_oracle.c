@@ -244,6 +244,18 @@ void or_schoolbook(uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t l
   for (uint64_t k = 0; k < n; ++k) c[k] = or_schoolbook_at(a, b, logn, q, (uint32_t)k);
 }
 
+/* Galois automorphism (Automorph):
+ * sigma_g(a)(x) = a(x^g) mod (x^N + 1) for odd g: coefficient i goes to
+ * i g mod 2N, negated when that exponent is >= N (x^N = -1). */
+void or_automorph(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, uint64_t g) {
+  uint64_t n = (uint64_t)1 << logn;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t t = (i * g) % (2 * n);
+    if (t < n) out[t] = a[i] % q;
+    else out[t - n] = or_submod(0, a[i] % q, q);
+  }
+}
+
 /* ---------------------------------------------------------- batch driver */
 /* Layout (reading C10): [batch][n_limbs][N], limb l uses moduli[l], psi[l].
  * op: 0 forward, 1 inverse, 2 polymul-with-eval-operand c = INTT(NTT(a) . b_hat),

@@ -462,3 +462,49 @@ def test_cfg3_seeded_digests():
     # sampled schoolbook at full size
     for k in (0, 12345, 65535):
         assert int(C[0, 0, k]) == O.schoolbook_at(a[0, 0], b[0, 0], mods[0], k)
+
+
+# ------------------------------------------------------------- automorph (f4)
+def test_automorph_monomials_closed_form():
+    """sigma_g(x^j) = x^{jg mod 2N}, with x^N = -1 (P:248 Automorph, P:194 ring)."""
+    q, logn = 97, 4
+    n = 1 << logn
+    for g in (1, 3, 5, 7, 31):
+        for j in range(n):
+            a = np.zeros(n, dtype=np.uint64)
+            a[j] = 1
+            out = O.automorph(a, q, g)
+            t = j * g % (2 * n)
+            want = np.zeros(n, dtype=np.uint64)
+            want[t % n] = 1 if t < n else q - 1
+            assert np.array_equal(out, want)
+
+
+def test_automorph_is_ring_homomorphism_and_composes():
+    q = 1152921504606830593
+    n = 64
+    rng = random.Random(3)
+    a = [rng.randrange(q) for _ in range(n)]
+    b = [rng.randrange(q) for _ in range(n)]
+    for g in (3, 5, 127):
+        lhs = O.automorph(schoolbook_py(a, b, q), q, g)
+        rhs = schoolbook_py(list(map(int, O.automorph(a, q, g))), list(map(int, O.automorph(b, q, g))), q)
+        assert list(map(int, lhs)) == rhs
+    for g, h in ((3, 5), (7, 9), (127, 3)):
+        assert np.array_equal(O.automorph(O.automorph(a, q, h), q, g), O.automorph(a, q, g * h % (2 * n)))
+    assert np.array_equal(O.automorph(a, q, 1), np.array(a, dtype=np.uint64))
+
+
+def test_automorph_ntt_domain_is_slot_permutation():
+    """NTT(sigma_g(a))[k] = NTT(a)[pi(k)], 2 brv(pi(k)) + 1 = (2 brv(k) + 1) g mod 2N."""
+    logn = 6
+    n = 1 << logn
+    q = O.primes(logn, 1)[0]
+    psi = O.min_psi(q, logn)
+    a = inputs.residues(5, 1, [q], n)[0, 0]
+    A = O.ntt_fwd(a, q, psi)
+    for g in (3, 5, 2 * n - 1):
+        S = O.ntt_fwd(O.automorph(a, q, g), q, psi)
+        for k in range(n):
+            e = (2 * brv_py(k, logn) + 1) * g % (2 * n)
+            assert int(S[k]) == int(A[brv_py((e - 1) // 2, logn)])
