@@ -105,6 +105,18 @@ rnt_status rnt_pointwise_mul(rnt_plan p, uint64_t* c, const uint64_t* a_hat,
 rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_t* b,
                        uint32_t batch, int b_is_eval, int b_broadcast, void* stream);
 
+/* Galois automorphism sigma_g: a(x) -> a(x^g) mod (x^N + 1), g odd, 0 < g < 2N
+ * (the Automorph operator of CKKS key switching / rotation; the
+ * rotation-ciphertext bank of HRF-MatVec).
+ *   ntt_domain == 0: coefficient form; coefficient i moves to i g mod 2N, negated
+ *                    when i g mod 2N >= N.
+ *   ntt_domain != 0: NTT form (the order of rnt_ntt_forward, reading C3); a pure
+ *                    permutation out[k] = in[pi(k)], 2 brv(pi(k)) + 1 = (2 brv(k) + 1) g mod 2N.
+ * out must not alias in (RNT_E_INVALID_ARG).  Layout, alignment, batch == 0 and
+ * stream rules as rnt_ntt_forward.  Even g or g >= 2N: RNT_E_INVALID_ARG. */
+rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, uint32_t galois_elt,
+                         int ntt_domain, void* stream);
+
 /* Operation codes for rnt_execute_host. */
 typedef enum {
   RNT_OP_FORWARD = 0,

@@ -28,11 +28,13 @@ from ._lib import (RNT_E_CUDA, RNT_E_INVALID_ARG, RNT_E_MODULUS, RNT_E_OOM, RNT_
                    status_string)
 
 __all__ = [
-    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "execute_host",
+    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "execute_host",
     "RntError", "status_string", "launch_count", "lib_path",
     "RNT_OK", "RNT_E_INVALID_ARG", "RNT_E_UNSUPPORTED_N", "RNT_E_MODULUS", "RNT_E_ROOT",
     "RNT_E_PLAN_MISMATCH", "RNT_E_CUDA", "RNT_E_OOM",
     "OP_FORWARD", "OP_INVERSE", "OP_POLYMUL_EVAL", "OP_POLYMUL",
+    "rnt_ntt_forward", "rnt_ntt_inverse", "rnt_pointwise_mul", "rnt_polymul", "rnt_automorph", "rnt_execute_host",
+    "rnt_status_string", "rnt_launch_count",
 ]
 
 OP_FORWARD, OP_INVERSE, OP_POLYMUL_EVAL, OP_POLYMUL = 0, 1, 2, 3
@@ -147,6 +149,13 @@ def polymul(plan: Plan, c, a, b_op, b_is_eval=False, batch=None, b_broadcast=Fal
                                   int(bool(b_broadcast)), _stream(stream)))
 
 
+def automorph(plan: Plan, out, inp, galois_elt: int, ntt_domain: bool = True, batch=None, stream=None) -> None:
+    """sigma_g: a(x) -> a(x^g) mod (x^N+1) (Automorph); NTT form is a slot permutation."""
+    b = _batch(plan, inp, batch)
+    _lib.check(_lib.L.rnt_automorph(plan.handle, _ptr(out), _ptr(inp), b, int(galois_elt), int(bool(ntt_domain)),
+                                    _stream(stream)))
+
+
 def execute_host(plan: Plan, op: int, out_host, in_host, dev_ws, b_dev=None, batch=None,
                  b_broadcast=False, stream=None) -> None:
     """Host buffers in/out (pinned recommended): H2D copy, op, D2H copy, async."""
@@ -156,3 +165,14 @@ def execute_host(plan: Plan, op: int, out_host, in_host, dev_ws, b_dev=None, bat
     bptr = _ptr(b_dev) if b_dev is not None else None
     _lib.check(_lib.L.rnt_execute_host(plan.handle, int(op), out_ptr, op_ptr, _ptr(dev_ws), bptr, hb,
                                        int(bool(b_broadcast)), _stream(stream)))
+
+
+# Aliases with the exact C-ABI names (include/rnsntt.h).
+rnt_ntt_forward = ntt_forward
+rnt_ntt_inverse = ntt_inverse
+rnt_pointwise_mul = pointwise_mul
+rnt_polymul = polymul
+rnt_automorph = automorph
+rnt_execute_host = execute_host
+rnt_status_string = status_string
+rnt_launch_count = launch_count

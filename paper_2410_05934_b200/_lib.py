@@ -27,6 +27,7 @@ SIGNATURES = {
     "rnt_ntt_inverse": (_i32, [_vp, _vp, _vp, _u32, _vp]),
     "rnt_pointwise_mul": (_i32, [_vp, _vp, _vp, _vp, _u32, _i32, _vp]),
     "rnt_polymul": (_i32, [_vp, _vp, _vp, _vp, _u32, _i32, _i32, _vp]),
+    "rnt_automorph": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _vp]),
     "rnt_execute_host": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _u32, _i32, _vp]),
     "rnt_status_string": (ctypes.c_char_p, [_i32]),
     "rnt_last_cuda_error": (_i32, []),
@@ -53,7 +54,19 @@ def _load():
     return lib
 
 
-L = _load()
+_L = None
+
+
+def __getattr__(name):
+    # The library is loaded on first use (PEP 562), so the package (and its
+    # build module) imports on a box where librnsntt.so is not built yet; any
+    # call into the library then raises ImportError -- there is no fallback.
+    global _L
+    if name == "L":
+        if _L is None:
+            _L = _load()
+        return _L
+    raise AttributeError(name)
 
 
 def lib_path() -> str:
@@ -61,7 +74,7 @@ def lib_path() -> str:
 
 
 def status_string(code: int) -> str:
-    s = L.rnt_status_string(int(code))
+    s = __getattr__("L").rnt_status_string(int(code))
     return s.decode() if s else f"rnt_status {code}"
 
 
@@ -69,9 +82,9 @@ def check(code: int) -> None:
     if code != RNT_OK:
         extra = ""
         if code in (RNT_E_CUDA, RNT_E_OOM):
-            extra = f" (cudaError {L.rnt_last_cuda_error()})"
+            extra = f" (cudaError {__getattr__('L').rnt_last_cuda_error()})"
         raise RntError(code, status_string(code) + extra)
 
 
 def launch_count() -> int:
-    return int(L.rnt_launch_count())
+    return int(__getattr__("L").rnt_launch_count())

@@ -98,6 +98,38 @@ __global__ void k_pointwise(u64* __restrict__ c, const u64* __restrict__ a, cons
   }
 }
 
+// Galois automorphism sigma_g (rnt_automorph).  One thread per output slot;
+// gathers from the same limb (L2-resident for N <= 2^16).
+//   NTT form:  out[k] = in[pi(k)],  2 brv(pi(k)) + 1 = (2 brv(k) + 1) g mod 2N
+//   coeff form: out[j] = +-in[j g^{-1} mod 2N] (sign when the source index >= N)
+__global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, const LimbC* __restrict__ lc,
+                            uint32_t L, uint32_t logn, uint32_t g, uint32_t ginv, int ntt_domain, uint64_t total) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t n = 1u << logn, mask2n = 2 * n - 1;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint64_t u = e >> logn;
+    const uint32_t k = (uint32_t)(e & (n - 1));
+    const u64* src = in + (u << logn);
+    u64 v;
+    if (ntt_domain) {
+      const uint32_t ek = 2u * (__brev(k) >> (32 - logn)) + 1u;          // odd exponent of slot k
+      const uint32_t es = (uint32_t)(((uint64_t)ek * g) & mask2n);       // times g mod 2N (odd)
+      const uint32_t kk = __brev((es - 1u) >> 1) >> (32 - logn);
+      v = __ldg(src + kk);
+    } else {
+      const uint32_t i0 = (uint32_t)(((uint64_t)k * ginv) & mask2n);
+      if (i0 < n) {
+        v = __ldg(src + i0);
+      } else {
+        const u64 x = __ldg(src + (i0 - n));
+        const u64 q = lc[u % L].q;
+        v = x ? q - x : 0ull;
+      }
+    }
+    out[e] = v;
+  }
+}
+
 static int g_num_sms = 0;
 static int num_sms() {
   if (!g_num_sms) {
@@ -544,6 +576,30 @@ rnt_status rnt_pointwise_mul(rnt_plan p, uint64_t* c, const uint64_t* a_hat, con
   k_pointwise<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<u64*>(c), reinterpret_cast<const u64*>(a_hat), reinterpret_cast<const u64*>(b_hat), b_broadcast ? 1 : 0, p->d_lc,
                                                                       p->L, p->logn, total2);
+  return after_launch();
+}
+
+rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, uint32_t galois_elt,
+                         int ntt_domain, void* stream) {
+  rnt_status s = check_data(p, out, in, batch);
+  if (s != RNT_OK || batch == 0) return s;
+  const uint32_t two_n = 2u << p->logn;
+  if (out == in || (galois_elt & 1u) == 0 || galois_elt >= two_n) return RNT_E_INVALID_ARG;
+  uint32_t ginv = 1;  // g^{-1} mod 2N: g^(N/2 - 1), the group (Z/2N)^* has exponent N/2 (N >= 4)
+  {
+    uint64_t b = galois_elt, e = (two_n / 4) - 1, r = 1;
+    for (; e; e >>= 1, b = b * b % two_n)
+      if (e & 1) r = r * b % two_n;
+    ginv = (uint32_t)r;
+  }
+  const uint64_t total = (uint64_t)batch * p->L << p->logn;
+  const int threads = 256;
+  uint64_t blocks = (total + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  k_automorph<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in), p->d_lc, p->L, p->logn, galois_elt, ginv,
+      ntt_domain ? 1 : 0, total);
   return after_launch();
 }
 

@@ -343,3 +343,47 @@ def test_kernel_variants(env):
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=600)
     assert "VARIANT_OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_bench_cfg5_step_exact_inputs():
+    """The exact bench.py cfg5 step (its input recipe and launch configuration),
+    every output element against the oracle."""
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for (logn, limbs, polys, seed) in bench.WORKLOADS["cfg5"]["parts"]:
+        mods, a, bhat = bench.make_part_inputs(logn, limbs, polys, seed, 0)
+        assert list(mods) == list(params(logn, limbs)[0])  # bench primes == reading C2
+        psi = [O.min_psi(q, logn) for q in mods]
+        p = R.Plan(logn, mods)
+        c = torch.empty(a.shape, dtype=torch.int64, device="cuda")
+        R.polymul(p, c, to_dev(a), to_dev(bhat), b_is_eval=True)
+        want = O.batch(O.OP_POLYMUL_EVAL, a, mods, psi, b=bhat, n_threads=8)
+        assert np.array_equal(from_dev(c), want)
+
+
+@pytest.mark.parametrize("logn,limbs,batch", [(4, 2, 3), (10, 1, 9), (12, 2, 2), (16, 3, 1)])
+def test_automorph_coeff_and_ntt_domain(logn, limbs, batch):
+    """rnt_automorph: coefficient form against the oracle definition,
+    NTT form against NTT(sigma_g(INTT(A)))."""
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    n = 1 << logn
+    a = inputs.residues(21, batch, ps, n)
+    A = O.batch(O.OP_FWD, a, ps, psi)
+    d = empty_dev(a.shape)
+    for g in (3, 5, 2 * n - 1, 5 ** 7 % (2 * n)):
+        R.automorph(p, d, to_dev(a), g, ntt_domain=False)
+        want = np.stack([np.stack([O.automorph(a[b, l], ps[l], g) for l in range(limbs)]) for b in range(batch)])
+        assert np.array_equal(from_dev(d), want)
+        R.automorph(p, d, to_dev(A), g, ntt_domain=True)
+        assert np.array_equal(from_dev(d), O.batch(O.OP_FWD, want, ps, psi))
+    with pytest.raises(R.RntError):
+        R.automorph(p, d, to_dev(a), 4)          # even Galois element
+    x = to_dev(a)
+    with pytest.raises(R.RntError):
+        R.automorph(p, x, x, 3)                  # aliasing
