@@ -509,6 +509,44 @@ def bench_latency(args):
                       "results": res}), flush=True)
 
 
+def bench_automorph(args):
+    """NTT-domain Galois automorphism on cfg3/cfg4 shapes; memory-bound,
+    roofline = HBM (16 B per element: read + write), L2 flushed between steps."""
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    res = {}
+    for wl in ("cfg3", "cfg4"):
+        (logn, limbs, polys, seed) = WORKLOADS[wl]["parts"][0]
+        mods = primes_for(logn, limbs)
+        plan = R.Plan(logn, mods)
+        a = torch.from_numpy(inputs.residues(seed, polys, mods, 1 << logn).view(np.int64)).cuda()
+        o = torch.empty_like(a)
+        g = 5 ** 3 % (2 << logn)
+        for _ in range(args.warmup):
+            R.automorph(plan, o, a, g, ntt_domain=True)
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            R.automorph(plan, o, a, g, ntt_domain=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = statistics.mean(ms)
+        gbs = a.numel() * 16 / (t * 1e-3) / 1e9
+        res[wl] = {"ms": t, "GBps": gbs, "frac_hbm": gbs / hbm}
+    print(json.dumps({"mode": "automorph", "metric": "NTT-domain Galois automorphism HBM GB/s",
+                      "roofline": {"bound": "hbm", "peak": hbm, "unit": "GB/s"}, "results": res}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -519,6 +557,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
+    ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -526,6 +565,8 @@ def main():
     parts = WORKLOADS[wl]["parts"]
     if args.latency:
         bench_latency(args)
+    elif args.automorph:
+        bench_automorph(args)
     elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:
