@@ -66,6 +66,8 @@ def _load():
                 "or_schoolbook_at": (u64, [_u64p, _u64p, u32, u64, u32]),
                 "or_schoolbook": (None, [_u64p, _u64p, _u64p, u32, u64]),
                 "or_automorph": (None, [_u64p, _u64p, u32, u64, u64]),
+                "or_decompose": (None, [_u64p, u64, u64, u32, u32]),
+                "or_external_product": (None, [_u64p, _u64p, _u64p, u32, u64, u64, u32, u32]),
                 "or_batch": (i32, [i32, _u64p, _u64p, i32, u32, u32, u32, _u64p, _u64p, i32]),
             }
             for name, (res, args) in sig.items():
@@ -202,6 +204,25 @@ def automorph(a, q: int, g: int) -> np.ndarray:
     a = _vec(a)
     out = np.zeros_like(a)
     _load().or_automorph(_p(out), _p(a), int(a.size).bit_length() - 1, q, g)
+    return out
+
+
+def decompose(v: int, q: int, base_log2: int, levels: int) -> list[int]:
+    """Signed gadget digits of v mod q as residues (Decompose)."""
+    out = np.zeros(levels, dtype=np.uint64)
+    _load().or_decompose(_p(out), v, q, base_log2, levels)
+    return [int(x) for x in out]
+
+
+def external_product(c, rgsw_hat, q: int, psi: int, base_log2: int, levels: int) -> np.ndarray:
+    """TFHE external product: c [2][N], rgsw_hat [2l][2][N] (NTT form) -> [2][N]."""
+    c = np.ascontiguousarray(c, dtype=np.uint64)
+    z = np.ascontiguousarray(rgsw_hat, dtype=np.uint64)
+    n = c.shape[-1]
+    assert c.shape == (2, n) and z.shape == (2 * levels, 2, n)
+    _check_canonical(c, q)
+    out = np.zeros_like(c)
+    _load().or_external_product(_p(out), _p(c), _p(z), n.bit_length() - 1, q, psi, base_log2, levels)
     return out
 
 

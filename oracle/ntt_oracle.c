@@ -256,6 +256,63 @@ void or_automorph(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, u
   }
 }
 
+/* Signed gadget decomposition (Decompose), reading G1:
+ * centre v in (-q/2, q/2]; digits d_0..d_{l-2} balanced in [-B/2, B/2),
+ * d_{l-1} takes the rest; sum_j d_j B^j = centred v exactly when B^l >= q.
+ * Digits are returned as residues mod q. */
+void or_decompose(uint64_t* digits, uint64_t v, uint64_t q, uint32_t base_log2, uint32_t levels) {
+  int64_t vc = (v > (q - 1) / 2) ? (int64_t)v - (int64_t)q : (int64_t)v;
+  const int64_t B = (int64_t)1 << base_log2;
+  for (uint32_t j = 0; j < levels; ++j) {
+    int64_t d;
+    if (j + 1 < levels) {
+      d = vc % B;               /* C remainder has the sign of vc */
+      if (d < 0) d += B;        /* mathematical vc mod B, in [0, B) */
+      if (d >= B / 2) d -= B;   /* balanced, in [-B/2, B/2) */
+      vc = (vc - d) / B;        /* exact division */
+    } else {
+      d = vc;                   /* last level keeps the remainder */
+    }
+    digits[j] = d >= 0 ? (uint64_t)d % q : q - (uint64_t)(-d) % q;
+  }
+}
+
+/* External product of TFHE (CMux building block):
+ * c = (c_0, c_1) an RLWE pair, rgsw_hat[r][i] (r < 2l, i < 2) RGSW rows in NTT
+ * form (the order of or_ntt_fwd).  D_{t,j} = digit j of c_t; r = t l + j;
+ *   out_i = INTT( sum_r NTT(D_r) (.) rgsw_hat[r][i] ),  i = 0, 1.
+ * c and out are [2][N]; rgsw_hat is [2l][2][N]. */
+void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat, uint32_t logn, uint64_t q,
+                         uint64_t psi, uint32_t base_log2, uint32_t levels) {
+  uint64_t n = (uint64_t)1 << logn;
+  uint64_t* fwd = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint64_t* inv = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint64_t ninv;
+  or_tables(q, psi, logn, fwd, inv, &ninv);
+  uint64_t* acc = (uint64_t*)calloc(2 * n, sizeof(uint64_t));
+  uint64_t* dig = (uint64_t*)malloc((size_t)levels * n * sizeof(uint64_t));
+  uint64_t* tmp = (uint64_t*)malloc(levels * sizeof(uint64_t));
+  for (uint32_t t = 0; t < 2; ++t) {
+    for (uint64_t k = 0; k < n; ++k) {
+      or_decompose(tmp, c[t * n + k], q, base_log2, levels);
+      for (uint32_t j = 0; j < levels; ++j) dig[j * n + k] = tmp[j];
+    }
+    for (uint32_t j = 0; j < levels; ++j) {
+      uint64_t* D = dig + (uint64_t)j * n;
+      or_ntt_fwd(D, logn, q, fwd);
+      uint64_t r = (uint64_t)t * levels + j;
+      for (uint32_t i = 0; i < 2; ++i)
+        for (uint64_t k = 0; k < n; ++k)
+          acc[i * n + k] = or_addmod(acc[i * n + k], or_mulmod(D[k], rgsw_hat[(r * 2 + i) * n + k], q), q);
+    }
+  }
+  for (uint32_t i = 0; i < 2; ++i) {
+    or_ntt_inv(acc + i * n, logn, q, inv, ninv);
+    memcpy(out + i * n, acc + i * n, n * sizeof(uint64_t));
+  }
+  free(fwd); free(inv); free(acc); free(dig); free(tmp);
+}
+
 /* ---------------------------------------------------------- batch driver */
 /* Layout (reading C10): [batch][n_limbs][N], limb l uses moduli[l], psi[l].
  * op: 0 forward, 1 inverse, 2 polymul-with-eval-operand c = INTT(NTT(a) . b_hat),

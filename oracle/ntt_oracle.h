@@ -27,6 +27,9 @@ uint64_t or_naive_intt_at(const uint64_t* A, uint32_t logn, uint64_t q, uint64_t
 uint64_t or_schoolbook_at(const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q, uint32_t k);
 void or_schoolbook(uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t logn, uint64_t q);
 void or_automorph(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, uint64_t g);
+void or_decompose(uint64_t* digits, uint64_t v, uint64_t q, uint32_t base_log2, uint32_t levels);
+void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat, uint32_t logn, uint64_t q,
+                         uint64_t psi, uint32_t base_log2, uint32_t levels);
 int or_batch(int op, uint64_t* data, const uint64_t* b, int b_bcast, uint32_t batch,
              uint32_t n_limbs, uint32_t logn, const uint64_t* moduli, const uint64_t* psi,
              int n_threads);

@@ -508,3 +508,68 @@ def test_automorph_ntt_domain_is_slot_permutation():
         for k in range(n):
             e = (2 * brv_py(k, logn) + 1) * g % (2 * n)
             assert int(S[k]) == int(A[brv_py((e - 1) // 2, logn)])
+
+
+# ------------------------------------------------ TFHE external product (f1)
+def test_decompose_spec_example():
+    # B_g=4, l=2, q=16, constant 7 -> digits (-1, 2): -1*1 + 2*4 = 7
+    d = O.decompose(7, 16, 2, 2)
+    assert d == [16 - 1, 2]
+
+
+def test_decompose_recomposes_exactly_and_digits_bounded():
+    rng = random.Random(17)
+    q = 1152921504606830593
+    for bg, l in ((20, 3), (15, 4), (10, 6), (30, 2)):
+        B = 1 << bg
+        assert B ** l >= q
+        vals = [0, 1, q - 1, (q - 1) // 2, (q + 1) // 2] + [rng.randrange(q) for _ in range(500)]
+        for v in vals:
+            ds = O.decompose(v, q, bg, l)
+            signed = [d if d <= q // 2 else d - q for d in ds]
+            assert all(-B // 2 <= s < B // 2 for s in signed[:-1])
+            assert -B // 2 <= signed[-1] <= B // 2
+            assert sum(s * B ** j for j, s in enumerate(signed)) % q == v
+
+
+def _gadget_rgsw_hat(q, psi, n, bg, l):
+    """Trivial RGSW of 1 with zero noise: row (t, j) = B^j e_t (gadget matrix G), NTT form."""
+    z = np.zeros((2 * l, 2, n), dtype=np.uint64)
+    for t in range(2):
+        for j in range(l):
+            row = np.zeros(n, dtype=np.uint64)
+            row[0] = pow(2, bg * j, q)
+            z[t * l + j, t] = O.ntt_fwd(row, q, psi)
+    return z
+
+
+def test_external_product_with_gadget_matrix_is_identity():
+    """Decompose-then-recompose is exact, so c boxtimes G = c."""
+    for logn, bg, l in ((4, 20, 3), (10, 20, 3), (10, 30, 2)):
+        n = 1 << logn
+        q = O.primes(logn, 1)[0]
+        psi = O.min_psi(q, logn)
+        c = inputs.residues(9, 2, [q], n)[:, 0, :]
+        out = O.external_product(c, _gadget_rgsw_hat(q, psi, n, bg, l), q, psi, bg, l)
+        assert np.array_equal(out, c)
+
+
+def test_external_product_matches_schoolbook_expansion():
+    logn, bg, l = 4, 20, 3
+    n = 1 << logn
+    q = O.primes(logn, 1)[0]
+    psi = O.min_psi(q, logn)
+    rng = np.random.default_rng(4)
+    c = inputs.residues(11, 2, [q], n)[:, 0, :]
+    z = inputs.residues(12, 2 * l * 2, [q], n).reshape(2 * l, 2, n)
+    zhat = np.stack([np.stack([O.ntt_fwd(z[r, i], q, psi) for i in range(2)]) for r in range(2 * l)])
+    out = O.external_product(c, zhat, q, psi, bg, l)
+    for i in range(2):
+        acc = [0] * n
+        for t in range(2):
+            digs = [O.decompose(int(v), q, bg, l) for v in c[t]]
+            for j in range(l):
+                D = [digs[k][j] for k in range(n)]
+                prod = schoolbook_py(D, list(map(int, z[t * l + j, i])), q)
+                acc = [(x + y) % q for x, y in zip(acc, prod)]
+        assert list(map(int, out[i])) == acc
