@@ -547,6 +547,63 @@ def bench_automorph(args):
                       "roofline": {"bound": "hbm", "peak": hbm, "unit": "GB/s"}, "results": res}), flush=True)
 
 
+def bench_extprod(args):
+    """TFHE external product, n_slot ciphertexts (N=2^10, k=1) against one
+    RGSW key (CMux-level batching), tab:tfhe parameters (1024, 630, 1, 3)
+    -> l = 3 levels, base 2^20 (exact decomposition for the 60-bit prime)."""
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    logn, l, bg = 10, 3, 20
+    n = 1 << logn
+    res = {}
+    mods = primes_for(logn, 1)
+    plan = R.Plan(logn, mods)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    for n_slot in (1024, 4096, 16384):
+        c = torch.from_numpy(inputs.residues(0, 2 * n_slot, mods, n).view(np.int64)).cuda()
+        z = torch.from_numpy(inputs.residues(1, 2 * l * 2, mods, n).view(np.int64)).cuda()
+        o = torch.empty_like(c)
+        for _ in range(args.warmup):
+            R.external_product(plan, o, c, z, bg, l, n_slot=n_slot)
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            R.external_product(plan, o, c, z, bg, l, n_slot=n_slot)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = statistics.mean(ms)
+        xf = n_slot * (2 * l + 2)
+        bf = xf * (n // 2) * logn
+        res[str(n_slot)] = {"ms": t, "external_products_per_s": n_slot / (t * 1e-3),
+                            "limb_transforms_per_s": xf / (t * 1e-3),
+                            "gbfly_per_s": bf / (t * 1e-3) / 1e9, "frac_alu": bf / (t * 1e-3) / 1e9 / peak_bfly}
+    # CPU oracle on a bounded sample
+    import oracle as O
+
+    cs = inputs.residues(0, 2 * 64, mods, n).reshape(64, 2, n)
+    zs = inputs.residues(1, 2 * l * 2, mods, n).reshape(2 * l, 2, n)
+    psi = O.min_psi(mods[0], logn)
+    t0 = time.perf_counter()
+    for sl in range(64):
+        O.external_product(cs[sl], zs, mods[0], psi, bg, l)
+    cpu = 64 / (time.perf_counter() - t0)
+    print(json.dumps({"mode": "external_product", "metric": "TFHE external products/s (N=2^10, l=3, B=2^20)",
+                      "roofline": {"bound": "alu", "peak": peak_bfly, "unit": "Gbutterfly/s"},
+                      "results": res,
+                      "cpu_baseline": {"value": cpu, "unit": "external products/s", "cores": 1, "kind": "oracle",
+                                       "sample": "64 slots, single thread"}}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -558,6 +615,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
     ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
+    ap.add_argument("--extprod", action="store_true", help="SURVEY f1 TFHE external product mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -567,6 +625,8 @@ def main():
         bench_latency(args)
     elif args.automorph:
         bench_automorph(args)
+    elif args.extprod:
+        bench_extprod(args)
     elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:

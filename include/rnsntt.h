@@ -117,6 +117,19 @@ rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_
 rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, uint32_t galois_elt,
                          int ntt_domain, void* stream);
 
+/* TFHE external product, batched over ciphertexts (P:164-166,
+ * CMux-level batching P:312-332).  Plan: 2^4 <= N <= 2^10 and n_limbs == 1
+ * (one NTT prime, reading C9).  For every slot s:
+ *   out[s][i] = INTT( sum_{t<2, j<l} NTT(D_{t,j}(c[s][t])) (.) rgsw_hat[t l + j][i] ),  i = 0, 1,
+ * with D_{t,j} the signed gadget digit j (base 2^base_log2, l = levels) of the
+ * centred coefficients of c[s][t] (digits j < l-1 balanced in [-B/2, B/2), the
+ * last keeps the remainder; exact when B^l >= q, reading G1 of DESIGN.md).
+ * c, out: device [n_slot][2][N]; rgsw_hat: device [2 l][2][N] in NTT form
+ * (rnt_ntt_forward order), shared by all slots.  out must not alias c.
+ * base_log2 in [1, 31], levels in [1, 8], base_log2 * (levels - 1) < 63. */
+rnt_status rnt_external_product(rnt_plan p, uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat,
+                                uint32_t n_slot, uint32_t base_log2, uint32_t levels, void* stream);
+
 /* Operation codes for rnt_execute_host. */
 typedef enum {
   RNT_OP_FORWARD = 0,

@@ -28,12 +28,14 @@ from ._lib import (RNT_E_CUDA, RNT_E_INVALID_ARG, RNT_E_MODULUS, RNT_E_OOM, RNT_
                    status_string)
 
 __all__ = [
-    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "execute_host",
+    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "external_product",
+    "execute_host",
     "RntError", "status_string", "launch_count", "lib_path",
     "RNT_OK", "RNT_E_INVALID_ARG", "RNT_E_UNSUPPORTED_N", "RNT_E_MODULUS", "RNT_E_ROOT",
     "RNT_E_PLAN_MISMATCH", "RNT_E_CUDA", "RNT_E_OOM",
     "OP_FORWARD", "OP_INVERSE", "OP_POLYMUL_EVAL", "OP_POLYMUL",
-    "rnt_ntt_forward", "rnt_ntt_inverse", "rnt_pointwise_mul", "rnt_polymul", "rnt_automorph", "rnt_execute_host",
+    "rnt_ntt_forward", "rnt_ntt_inverse", "rnt_pointwise_mul", "rnt_polymul", "rnt_automorph",
+    "rnt_external_product", "rnt_execute_host",
     "rnt_status_string", "rnt_launch_count",
 ]
 
@@ -156,6 +158,15 @@ def automorph(plan: Plan, out, inp, galois_elt: int, ntt_domain: bool = True, ba
                                     _stream(stream)))
 
 
+def external_product(plan: Plan, out, c, rgsw_hat, base_log2: int, levels: int, n_slot=None,
+                     stream=None) -> None:
+    """TFHE external product of n_slot RLWE pairs with one RGSW key in NTT form
+    (CMux-level batching P:324-332): out, c [n_slot][2][N]; rgsw_hat [2l][2][N]."""
+    ns = int(n_slot) if n_slot is not None else c.numel() // (2 * plan.n)
+    _lib.check(_lib.L.rnt_external_product(plan.handle, _ptr(out), _ptr(c), _ptr(rgsw_hat), ns, int(base_log2),
+                                           int(levels), _stream(stream)))
+
+
 def execute_host(plan: Plan, op: int, out_host, in_host, dev_ws, b_dev=None, batch=None,
                  b_broadcast=False, stream=None) -> None:
     """Host buffers in/out (pinned recommended): H2D copy, op, D2H copy, async."""
@@ -173,6 +184,7 @@ rnt_ntt_inverse = ntt_inverse
 rnt_pointwise_mul = pointwise_mul
 rnt_polymul = polymul
 rnt_automorph = automorph
+rnt_external_product = external_product
 rnt_execute_host = execute_host
 rnt_status_string = status_string
 rnt_launch_count = launch_count

@@ -382,6 +382,21 @@ static rnt_status check_data(const rnt_plan_s* p, const void* a, const void* b, 
 }
 
 // --------------------------------------------------------------------- ABI
+template <int LOGN>
+static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
+                                 DigitSpec ds, cudaStream_t st) {
+  static bool attr_set = false;  // benign race: idempotent attribute call
+  const size_t smem = (size_t)2 * 3 * kWarpBuf * 8;
+  if (!attr_set) {
+    RNT_CUDA(cudaFuncSetAttribute(k_extprod<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const uint64_t per_cta = 2ull * (kWarpElems >> LOGN);
+  const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
+  k_extprod<LOGN><<<(unsigned)grid, 64, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc, n_slot, ds);
+  return after_launch();
+}
+
 extern "C" {
 
 const char* rnt_status_string(rnt_status s) {
@@ -601,6 +616,39 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
       reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in), p->d_lc, p->L, p->logn, galois_elt, ginv,
       ntt_domain ? 1 : 0, total);
   return after_launch();
+}
+
+rnt_status rnt_external_product(rnt_plan p, uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat,
+                                uint32_t n_slot, uint32_t base_log2, uint32_t levels, void* stream) {
+  if (!p) return RNT_E_INVALID_ARG;
+  if (n_slot == 0) return RNT_OK;
+  if (p->L != 1 || p->logn > 10) return RNT_E_INVALID_ARG;
+  if (!out || !c || !rgsw_hat || out == c || !aligned16(out) || !aligned16(c) || !aligned16(rgsw_hat))
+    return RNT_E_INVALID_ARG;
+  if (base_log2 < 1 || base_log2 > 31 || levels < 1 || levels > 8 || base_log2 * (levels - 1) >= 63)
+    return RNT_E_INVALID_ARG;
+  rnt_status s = check_plan_device(p);
+  if (s != RNT_OK) return s;
+  DigitSpec ds;
+  ds.bg = base_log2;
+  ds.levels = levels;
+  ds.off = 0;
+  for (uint32_t i = 0; i + 1 < levels; ++i) ds.off += ((int64_t)1 << (base_log2 - 1)) << (i * base_log2);
+  ds.half_q = (p->limbs[0].q - 1) / 2;
+  u64* o = reinterpret_cast<u64*>(out);
+  const u64* ci = reinterpret_cast<const u64*>(c);
+  const u64* z = reinterpret_cast<const u64*>(rgsw_hat);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (p->logn) {
+    case 4: return launch_extprod<4>(p, o, ci, z, n_slot, ds, st);
+    case 5: return launch_extprod<5>(p, o, ci, z, n_slot, ds, st);
+    case 6: return launch_extprod<6>(p, o, ci, z, n_slot, ds, st);
+    case 7: return launch_extprod<7>(p, o, ci, z, n_slot, ds, st);
+    case 8: return launch_extprod<8>(p, o, ci, z, n_slot, ds, st);
+    case 9: return launch_extprod<9>(p, o, ci, z, n_slot, ds, st);
+    case 10: return launch_extprod<10>(p, o, ci, z, n_slot, ds, st);
+  }
+  return RNT_E_UNSUPPORTED_N;
 }
 
 rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_t* b, uint32_t batch, int b_is_eval,

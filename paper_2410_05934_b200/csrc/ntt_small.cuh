@@ -512,6 +512,132 @@ inline size_t warp_tma_smem_bytes() {
   return (size_t)W * (kWarpElems + kWarpBuf + 2) * 8;
 }
 
+
+// ---- TFHE external product ---------------------------------
+// c [n_slot][2][N] (RLWE pairs, one prime), rgsw_hat [2l][2][N] (NTT form, shared
+// by all slots -- the CMux-level batching of P:324-332 applies one RGSW key to
+// n_slot ciphertexts), out [n_slot][2][N]:
+//   out_i = INTT( sum_{t,j} NTT(D_{t,j}) (.) rgsw_hat[t l + j][i] ),
+// D_{t,j} = signed gadget digit j of c_t (Decompose).  Per warp: the
+// digit is formed while the first pass loads c_t; the last forward pass
+// multiplies (Montgomery) and accumulates into two shared-memory accumulators;
+// two inverse transforms (N^{-1} 2^64 scale) write the output pair.
+struct DigitSpec {
+  uint32_t bg, levels;
+  int64_t off;     // sum_{i < l-1} (B/2) B^i
+  u64 half_q;      // (q - 1) / 2
+};
+
+__device__ __forceinline__ u64 gadget_digit(u64 v, u64 q, const DigitSpec& ds, uint32_t j) {
+  const int64_t vc = v > ds.half_q ? (int64_t)v - (int64_t)q : (int64_t)v;   // centred
+  const int64_t u = vc + ds.off;
+  int64_t d;
+  if (j + 1 < ds.levels) {
+    const int64_t B = (int64_t)1 << ds.bg;
+    d = ((u >> (j * ds.bg)) & (B - 1)) - (B >> 1);   // balanced digit
+  } else {
+    d = u >> (j * ds.bg);                           // last level: the remainder
+  }
+  return d >= 0 ? (u64)d : q - (u64)(-d);
+}
+
+// first forward pass of digit j of component view `src`
+template <int LOGN, int S, int K>
+__device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, const TW* T, u64 q, u64 q2,
+                                               const DigitSpec& ds, uint32_t j) {
+  using Geo = PassGeo<LOGN, S, K>;
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int gi = 0; gi < Geo::GPL; ++gi) {
+    const Geo g(lane + 32 * gi);
+    const int jj0 = g.base - g.poly * N;
+    const int pb = wpad(g.base);
+    const bool live = src.live(g.poly);
+    const u64* sp = src.at(g.poly) + jj0;
+    u64 x[1 << K];
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) x[i] = live ? gadget_digit(sp[i * Geo::LO], q, ds, j) : 0ull;
+    ct_group<S, K>(x, T, g.hi, q, q2);
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
+  }
+  __syncwarp();
+}
+
+// last forward pass: CT stages, then acc_i += x (.) z_i (i = 0, 1), kept in [0, 2q)
+template <int LOGN, int S, int K>
+__device__ __forceinline__ void fwd_pass_mac(u64* buf, u64* acc0, u64* acc1, const u64* z0, const u64* z1, int lane,
+                                             const TW* T, u64 q, u64 q2, u64 qinv) {
+  using Geo = PassGeo<LOGN, S, K>;
+  constexpr int N = 1 << LOGN;
+#pragma unroll 1
+  for (int gi = 0; gi < Geo::GPL; ++gi) {
+    const Geo g(lane + 32 * gi);
+    const int jj0 = g.base - g.poly * N;
+    const int pb = wpad(g.base);
+    u64 x[1 << K];
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
+    ct_group<S, K>(x, T, g.hi, q, q2);
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) {
+      const int o = pb + pad_off<LOGN, S, Geo::LO>(i);
+      const int e = jj0 + i * Geo::LO;
+      acc0[o] = csub(acc0[o] + mont_mul(x[i], __ldg(z0 + e), q, qinv), q2);
+      acc1[o] = csub(acc1[o] + mont_mul(x[i], __ldg(z1 + e), q, qinv), q2);
+    }
+  }
+  __syncwarp();
+}
+
+template <int LOGN, int KM = 3>
+__global__ void __launch_bounds__(2 * 32, 8)
+k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restrict__ zhat,
+          const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
+          uint32_t n_slot, DigitSpec ds) {
+  using PS = Passes<LOGN, KM>;
+  constexpr int N = 1 << LOGN;
+  constexpr int P = kWarpElems / N;
+  constexpr int NP = PS::NP;
+  static_assert(NP >= 2, "N >= 16");
+  extern __shared__ __align__(16) u64 smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t s0 = ((uint64_t)blockIdx.x * 2 + warp) * P;
+  if (s0 >= n_slot) return;
+  u64* buf = smem + (size_t)warp * 3 * kWarpBuf;
+  u64* acc0 = buf + kWarpBuf;
+  u64* acc1 = acc0 + kWarpBuf;
+  for (int i = lane; i < kWarpBuf; i += 32) {
+    acc0[i] = 0;
+    acc1[i] = 0;
+  }
+  __syncwarp();
+  const u64 q = lc[0].q, q2 = lc[0].q2, qinv = lc[0].qinv;
+  for (uint32_t t = 0; t < 2; ++t) {
+    const GView cv{c + (uint64_t)t * N, s0, 2ull * N, n_slot};
+    for (uint32_t j = 0; j < ds.levels; ++j) {
+      const uint64_t r = (uint64_t)t * ds.levels + j;
+      fwd_pass_digit<LOGN, 0, PS::k(0)>(buf, cv, lane, tw_fwd, q, q2, ds, j);
+      sfor<1, NP - 1>([&](auto P_) {
+        constexpr int p = decltype(P_)::value;
+        fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf>(buf, cv, cv, lane, tw_fwd, q, q2);
+      });
+      fwd_pass_mac<LOGN, PS::s(NP - 1), PS::k(NP - 1)>(buf, acc0, acc1, zhat + (r * 2 + 0) * N, zhat + (r * 2 + 1) * N,
+                                                       lane, tw_fwd, q, q2, qinv);
+    }
+  }
+  const TW s0w = lc[0].ninvR, s1w = lc[0].ninvR_w1;
+  for (uint32_t i = 0; i < 2; ++i) {
+    u64* acc = i ? acc1 : acc0;
+    const GView ov{out + (uint64_t)i * N, s0, 2ull * N, n_slot};
+    sfor<0, NP>([&](auto I_) {
+      constexpr int p = NP - 1 - decltype(I_)::value;
+      inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(acc, ov, ov, lane, tw_inv, s0w, s1w, q, q2);
+    });
+  }
+}
+
 template <int LOGN, int MODE, int W = kTeamWarps>
 inline size_t warp_smem_bytes() {
   return (size_t)W * kWarpBuf * 8 * (MODE == 3 ? 2 : 1);

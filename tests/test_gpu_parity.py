@@ -387,3 +387,31 @@ def test_automorph_coeff_and_ntt_domain(logn, limbs, batch):
     x = to_dev(a)
     with pytest.raises(R.RntError):
         R.automorph(p, x, x, 3)                  # aliasing
+
+
+@pytest.mark.parametrize("logn,n_slot,bg,l", [(10, 37, 20, 3), (10, 64, 30, 2), (10, 5, 10, 6), (6, 50, 20, 3),
+                                              (4, 70, 15, 4)])
+def test_external_product(logn, n_slot, bg, l):
+    """rnt_external_product bit-exact against the oracle, plus the
+    gadget-matrix identity c boxtimes G = c."""
+    ps, psi = params(logn, 1)
+    q, pi = ps[0], psi[0]
+    n = 1 << logn
+    p = R.Plan(logn, ps)
+    c = inputs.residues(31, 2 * n_slot, [q], n).reshape(n_slot, 2, n)
+    z = inputs.residues(32, 2 * l * 2, [q], n).reshape(2 * l, 2, n)   # uniform NTT-form key rows
+    d = empty_dev(c.shape)
+    R.external_product(p, d, to_dev(c), to_dev(z), bg, l)
+    got = from_dev(d)
+    for s in range(n_slot):
+        assert np.array_equal(got[s], O.external_product(c[s], z, q, pi, bg, l))
+    # identity with the trivial gadget RGSW (exact decomposition: B^l >= q)
+    if (1 << bg) ** l >= q:
+        G = np.zeros((2 * l, 2, n), dtype=np.uint64)
+        for t in range(2):
+            for j in range(l):
+                row = np.zeros(n, dtype=np.uint64)
+                row[0] = pow(2, bg * j, q)
+                G[t * l + j, t] = O.ntt_fwd(row, q, pi)
+        R.external_product(p, d, to_dev(c), to_dev(G), bg, l)
+        assert np.array_equal(from_dev(d), c)
