@@ -130,16 +130,6 @@ void plan_powers(const HostLimb& lm, uint32_t logn, bool inverse, uint32_t count
   for (uint32_t i = 0; i < count; ++i) tab[i] = make_tw(pw[hp_bitrev(i, logn)], q);
 }
 
-void plan_team_layout(const HostTW* nat, uint32_t logn, HostTW* out) {
-  const uint32_t n = 1u << logn, G = logn / 2, S = 1u << G, e = logn - G, E = 1u << e;
-  std::memset(out, 0, sizeof(HostTW) * n);
-  for (uint32_t i = 1; i < E; ++i) out[i] = nat[i];
-  for (uint32_t s = e; s < logn; ++s)
-    for (uint32_t lam = 0; lam < S; ++lam)
-      for (uint32_t m = 0; m < (1u << (s - G)); ++m)
-        out[(1u << s) + m * S + lam] = nat[(1u << s) + lam * (1u << (s - G)) + m];
-}
-
 void plan_row_layout(const HostTW* nat, uint32_t logn, HostTW* out) {
   const uint32_t n1 = (logn + 1) / 2, n2 = logn / 2, R = 1u << n1, Cn = 1u << n2, T2 = Cn / 16;
   std::memset(out, 0, sizeof(HostTW) * (size_t)R * Cn);

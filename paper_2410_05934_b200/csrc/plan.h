@@ -35,10 +35,9 @@ int plan_limbs(uint32_t logn, uint32_t L, const uint64_t* moduli, const uint64_t
 // each with its Shoup companion.
 void plan_powers(const HostLimb& lm, uint32_t logn, bool inverse, uint32_t count, HostTW* tab);
 
-// Kernel layouts (see ntt_small.cuh / ntt_large.cuh):
-//   team layout (N <= 2^10), N entries; row layout (N >= 2^11), N entries;
-//   column layout = first 2^{n1} natural entries.
-void plan_team_layout(const HostTW* natural, uint32_t logn, HostTW* out);
+// Kernel layouts (see ntt_small.cuh / ntt_large.cuh): N <= 2^10 uses the
+// natural order; N >= 2^11 uses a lane-major row layout (k_row), a natural
+// per-row layout (k_rows) and the first 2^{n1} natural entries (columns).
 void plan_row_layout(const HostTW* natural, uint32_t logn, HostTW* out);
 // Natural per-row layout for the warp-engine row kernel (k_rows):
 // out[r 2^{n2} + 2^v + j] = natural[2^{n1+v} + r 2^v + j].
