@@ -68,6 +68,7 @@ def _load():
                 "or_automorph": (None, [_u64p, _u64p, u32, u64, u64]),
                 "or_decompose": (None, [_u64p, u64, u64, u32, u32]),
                 "or_external_product": (None, [_u64p, _u64p, _u64p, u32, u64, u64, u32, u32]),
+                "or_bconv": (None, [_u64p, _u64p, u64, _u64p, u32, _u64p, u32]),
                 "or_batch": (i32, [i32, _u64p, _u64p, i32, u32, u32, u32, _u64p, _u64p, i32]),
             }
             for name, (res, args) in sig.items():
@@ -223,6 +224,19 @@ def external_product(c, rgsw_hat, q: int, psi: int, base_log2: int, levels: int)
     _check_canonical(c, q)
     out = np.zeros_like(c)
     _load().or_external_product(_p(out), _p(c), _p(z), n.bit_length() - 1, q, psi, base_log2, levels)
+    return out
+
+
+def bconv(x, q_basis, p_basis) -> np.ndarray:
+    """Fast basis conversion Q -> P (BConv): x [L][N] -> [K][N]."""
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    L, n = x.shape
+    qs, ps = _vec(q_basis), _vec(p_basis)
+    assert qs.size == L
+    for i in range(L):
+        _check_canonical(x[i], int(qs[i]))
+    out = np.zeros((ps.size, n), dtype=np.uint64)
+    _load().or_bconv(_p(out), _p(x), n, _p(qs), L, _p(ps), ps.size)
     return out
 
 

@@ -313,6 +313,41 @@ void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_
   free(fwd); free(inv); free(acc); free(dig); free(tmp);
 }
 
+/* Fast basis conversion BConv (CKKS key switching ModUp / ModDown, P:247-248;
+ * SPEC S:82-90): from basis Q = {q_0..q_{L-1}} to P = {p_0..p_{K-1}},
+ * per coefficient (reading G3):
+ *   y_i   = x_i * (Q/q_i)^{-1} mod q_i
+ *   out_j = sum_i y_i * (Q/q_i mod p_j) mod p_j      (= X + alpha Q mod p_j, 0 <= alpha < L)
+ * in: [L][N] residues, out: [K][N]. */
+void or_bconv(uint64_t* out, const uint64_t* in, uint64_t n, const uint64_t* q, uint32_t L, const uint64_t* p,
+              uint32_t K) {
+  uint64_t* qhat_inv = (uint64_t*)malloc(L * sizeof(uint64_t));
+  uint64_t* qhat_p = (uint64_t*)malloc((size_t)L * K * sizeof(uint64_t));
+  for (uint32_t i = 0; i < L; ++i) {
+    uint64_t h = 1 % q[i];
+    for (uint32_t k = 0; k < L; ++k)
+      if (k != i) h = or_mulmod(h, q[k] % q[i], q[i]);
+    qhat_inv[i] = or_powmod(h, q[i] - 2, q[i]);
+    for (uint32_t j = 0; j < K; ++j) {
+      uint64_t hp = 1 % p[j];
+      for (uint32_t k = 0; k < L; ++k)
+        if (k != i) hp = or_mulmod(hp, q[k] % p[j], p[j]);
+      qhat_p[(size_t)i * K + j] = hp;
+    }
+  }
+  uint64_t* y = (uint64_t*)malloc(L * sizeof(uint64_t));
+  for (uint64_t c = 0; c < n; ++c) {
+    for (uint32_t i = 0; i < L; ++i) y[i] = or_mulmod(in[(size_t)i * n + c], qhat_inv[i], q[i]);
+    for (uint32_t j = 0; j < K; ++j) {
+      uint64_t acc = 0;
+      for (uint32_t i = 0; i < L; ++i)
+        acc = or_addmod(acc, or_mulmod(y[i] % p[j], qhat_p[(size_t)i * K + j], p[j]), p[j]);
+      out[(size_t)j * n + c] = acc;
+    }
+  }
+  free(qhat_inv); free(qhat_p); free(y);
+}
+
 /* ---------------------------------------------------------- batch driver */
 /* Layout (reading C10): [batch][n_limbs][N], limb l uses moduli[l], psi[l].
  * op: 0 forward, 1 inverse, 2 polymul-with-eval-operand c = INTT(NTT(a) . b_hat),

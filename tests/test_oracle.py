@@ -573,3 +573,50 @@ def test_external_product_matches_schoolbook_expansion():
                 prod = schoolbook_py(D, list(map(int, z[t * l + j, i])), q)
                 acc = [(x + y) % q for x, y in zip(acc, prod)]
         assert list(map(int, out[i])) == acc
+
+
+# ---------------------------------------------------------------- BConv (f2)
+def _crt(residues, mods):
+    M = 1
+    for m in mods:
+        M *= m
+    x = 0
+    for r, m in zip(residues, mods):
+        Mi = M // m
+        x += int(r) * Mi * pow(Mi, -1, m)
+    return x % M, M
+
+
+def test_bconv_is_x_plus_alpha_q_with_alpha_below_L():
+    """BConv = X + alpha Q (0 <= alpha < L) with X the exact CRT value (big ints)."""
+    qs = O.primes(10, 5)
+    ps = O.primes(11, 4)   # disjoint basis (q = 1 mod 2^12)
+    rng = random.Random(5)
+    n = 16
+    x = np.array([[rng.randrange(q) for _ in range(n)] for q in qs], dtype=np.uint64)
+    x[:, 0] = 0
+    x[:, 1] = [q - 1 for q in qs]
+    out = O.bconv(x, qs, ps)
+    Q = 1
+    for q in qs:
+        Q *= q
+    for c in range(n):
+        X, _ = _crt(x[:, c], qs)
+        ys = [int(x[i, c]) * pow(Q // qs[i], -1, qs[i]) % qs[i] for i in range(len(qs))]
+        S = sum(y * (Q // q) for y, q in zip(ys, qs))
+        alpha = (S - X) // Q
+        assert (S - X) % Q == 0 and 0 <= alpha < len(qs)
+        for j, p in enumerate(ps):
+            assert int(out[j, c]) == (X + alpha * Q) % p
+
+
+def test_bconv_zero_and_single_limb():
+    """x = 0 maps to 0; with L = 1 (Q = q_0, alpha = 0) BConv is x mod p_j exactly."""
+    qs = O.primes(10, 3)
+    ps = O.primes(11, 2)
+    x = np.zeros((3, 4), dtype=np.uint64)
+    assert not O.bconv(x, qs, ps).any()
+    x1 = np.array([[5, qs[0] - 1, 123456789, 0]], dtype=np.uint64)
+    out = O.bconv(x1, qs[:1], ps)
+    for j, p in enumerate(ps):
+        assert list(map(int, out[j])) == [int(v) % p for v in x1[0]]
