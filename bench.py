@@ -604,6 +604,53 @@ def bench_extprod(args):
                                        "sample": "64 slots, single thread"}}), flush=True)
 
 
+def bench_modup(args):
+    """CKKS ModUp of one key-switching digit at N=2^16 (dnum = 3 for L = 45:
+    a 15-limb digit extended to the other 30 limbs + 15 special primes):
+    INTT (15 limbs) -> BConv (15 -> 45) -> NTT (45 limbs); L2 flushed between steps."""
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    logn, Lin, Kout = 16, 15, 45
+    mods = primes_for(logn, Lin + Kout)
+    src, dst = mods[:Lin], mods[Lin:]
+    ps, pd = R.Plan(logn, src), R.Plan(logn, dst)
+    bc = R.BConv(ps, pd)
+    a = torch.from_numpy(inputs.residues(0, 1, src, 1 << logn).view(np.int64)).cuda()
+    coeff = torch.empty_like(a)
+    ext = torch.empty((1, Kout, 1 << logn), dtype=torch.int64, device="cuda")
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def step(ev):
+        ev[0].record()
+        R.ntt_inverse(ps, coeff, a)
+        ev[1].record()
+        bc(ext, coeff)
+        ev[2].record()
+        R.ntt_forward(pd, ext, ext)
+        ev[3].record()
+
+    for _ in range(args.warmup):
+        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    parts = [[], [], []]
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        step(ev)
+        torch.cuda.synchronize()
+        for k in range(3):
+            parts[k].append(ev[k].elapsed_time(ev[k + 1]))
+    ms = [statistics.mean(x) for x in parts]
+    n = 1 << logn
+    print(json.dumps({"mode": "modup", "metric": "CKKS ModUp of one digit (INTT -> BConv -> NTT), N=2^16",
+                      "config": {"digit_limbs": Lin, "target_limbs": Kout},
+                      "ms": {"intt": ms[0], "bconv": ms[1], "ntt": ms[2], "total": sum(ms)},
+                      "bconv_modmul_per_s": n * Lin * (Kout + 1) / (ms[1] * 1e-3),
+                      "limb_transforms_per_s": (Lin + Kout) / (ms[0] * 1e-3 + ms[2] * 1e-3)}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -616,6 +663,7 @@ def main():
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
     ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
     ap.add_argument("--extprod", action="store_true", help="SURVEY f1 TFHE external product mode")
+    ap.add_argument("--modup", action="store_true", help="SURVEY f2 CKKS ModUp (INTT -> BConv -> NTT) mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -627,6 +675,8 @@ def main():
         bench_automorph(args)
     elif args.extprod:
         bench_extprod(args)
+    elif args.modup:
+        bench_modup(args)
     elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:

@@ -130,6 +130,18 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
 rnt_status rnt_external_product(rnt_plan p, uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat,
                                 uint32_t n_slot, uint32_t base_log2, uint32_t levels, void* stream);
 
+/* Fast basis conversion BConv (CKKS key switching ModUp / ModDown, P:247-248;
+ * SPEC S:82-90) from the basis Q of plan `from` (L limbs) to
+ * the basis P of plan `to` (K limbs), same N and device.  Per coefficient:
+ *   y_i = x_i (Q/q_i)^{-1} mod q_i,   out_j = sum_i y_i (Q/q_i mod p_j) mod p_j
+ * (= X + alpha Q mod p_j with X the CRT value and 0 <= alpha < L).  Coefficient
+ * form in and out: in [batch][L][N], out [batch][K][N], device, 16-byte aligned,
+ * out must not alias in.  The context owns its device tables; L <= 192. */
+typedef struct rnt_bconv_s* rnt_bconv;
+rnt_status rnt_bconv_create(rnt_bconv* out, rnt_plan from, rnt_plan to);
+rnt_status rnt_bconv_destroy(rnt_bconv c);
+rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream);
+
 /* Operation codes for rnt_execute_host. */
 typedef enum {
   RNT_OP_FORWARD = 0,

@@ -28,7 +28,7 @@ from ._lib import (RNT_E_CUDA, RNT_E_INVALID_ARG, RNT_E_MODULUS, RNT_E_OOM, RNT_
                    status_string)
 
 __all__ = [
-    "Plan", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "external_product",
+    "Plan", "BConv", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "external_product",
     "execute_host",
     "RntError", "status_string", "launch_count", "lib_path",
     "RNT_OK", "RNT_E_INVALID_ARG", "RNT_E_UNSUPPORTED_N", "RNT_E_MODULUS", "RNT_E_ROOT",
@@ -165,6 +165,31 @@ def external_product(plan: Plan, out, c, rgsw_hat, base_log2: int, levels: int, 
     ns = int(n_slot) if n_slot is not None else c.numel() // (2 * plan.n)
     _lib.check(_lib.L.rnt_external_product(plan.handle, _ptr(out), _ptr(c), _ptr(rgsw_hat), ns, int(base_log2),
                                            int(levels), _stream(stream)))
+
+
+class BConv:
+    """Fast basis conversion Q (plan `src`) -> P (plan `dst`) (BConv)."""
+
+    def __init__(self, src: Plan, dst: Plan):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.L.rnt_bconv_create(ctypes.byref(h), src.handle, dst.handle))
+        self._h = h
+        self.src, self.dst = src, dst
+
+    def __call__(self, out, inp, batch=None, stream=None) -> None:
+        b = int(batch) if batch is not None else inp.numel() // (self.src.n_limbs * self.src.n)
+        _lib.check(_lib.L.rnt_bconv_apply(self._h, _ptr(out), _ptr(inp), b, _stream(stream)))
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.L.rnt_bconv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
 
 
 def execute_host(plan: Plan, op: int, out_host, in_host, dev_ws, b_dev=None, batch=None,

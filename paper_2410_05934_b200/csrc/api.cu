@@ -130,6 +130,43 @@ __global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, c
   }
 }
 
+// Fast basis conversion (rnt_bconv_apply).  A CTA converts kBcTile coefficient
+// positions of one polynomial: phase 1 computes y_i = x_i qhat_i^{-1} mod q_i
+// into shared memory, phase 2 accumulates out_j = sum_i y_i (qhat_i mod p_j)
+// with Shoup products w.r.t. p_j (lazy [0, 2p_j), one conditional subtraction
+// per term), canonical output.
+constexpr int kBcTile = 128;
+struct BcMod {
+  u64 m, m2;
+  TW qhatinv;  // only for source limbs
+};
+
+__global__ void __launch_bounds__(kBcTile)
+k_bconv(u64* __restrict__ out, const u64* __restrict__ in, const BcMod* __restrict__ src, const BcMod* __restrict__ dst,
+        const TW* __restrict__ qhat_p, uint32_t L, uint32_t K, uint32_t logn) {
+  extern __shared__ __align__(16) u64 ys[];   // [L][kBcTile]
+  const uint32_t n = 1u << logn;
+  const uint64_t b = blockIdx.y;
+  const uint32_t c = blockIdx.x * kBcTile + threadIdx.x;
+  const bool live = c < n;
+  const u64* x = in + (b * L << logn) + (live ? c : 0);
+  for (uint32_t i = 0; i < L; ++i) {
+    const u64 q = src[i].m;
+    ys[i * kBcTile + threadIdx.x] = csub(shoup_lazy(__ldg(x + ((uint64_t)i << logn)), src[i].qhatinv, q), q);
+  }
+  __syncthreads();
+  if (!live) return;
+  u64* o = out + (b * K << logn) + c;
+  for (uint32_t j = 0; j < K; ++j) {
+    const u64 p = dst[j].m, p2 = dst[j].m2;
+    const TW* row = qhat_p + (size_t)j * L;
+    u64 acc = 0;
+#pragma unroll 4
+    for (uint32_t i = 0; i < L; ++i) acc = csub(acc + shoup_lazy(ys[i * kBcTile + threadIdx.x], ldg_tw(row + i), p), p2);
+    o[(uint64_t)j << logn] = csub(acc, p);
+  }
+}
+
 static int g_num_sms = 0;
 static int num_sms() {
   if (!g_num_sms) {
@@ -382,6 +419,14 @@ static rnt_status check_data(const rnt_plan_s* p, const void* a, const void* b, 
 }
 
 // --------------------------------------------------------------------- ABI
+struct rnt_bconv_s {
+  int device = 0;
+  uint32_t logn = 0, L = 0, K = 0;
+  BcMod* d_src = nullptr;
+  BcMod* d_dst = nullptr;
+  TW* d_qhat_p = nullptr;   // [K][L]: Shoup pair of (Q/q_i mod p_j) w.r.t. p_j
+};
+
 template <int LOGN>
 static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                  DigitSpec ds, cudaStream_t st) {
@@ -615,6 +660,87 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
   k_automorph<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in), p->d_lc, p->L, p->logn, galois_elt, ginv,
       ntt_domain ? 1 : 0, total);
+  return after_launch();
+}
+
+rnt_status rnt_bconv_create(rnt_bconv* out, rnt_plan from, rnt_plan to) {
+  if (!out || !from || !to) return RNT_E_INVALID_ARG;
+  *out = nullptr;
+  if (from->logn != to->logn || from->device != to->device || from->L > 192) return RNT_E_INVALID_ARG;
+  rnt_status s = check_plan_device(from);
+  if (s != RNT_OK) return s;
+  const uint32_t L = from->L, K = to->L;
+  std::vector<BcMod> src(L), dst(K);
+  std::vector<TW> qp((size_t)K * L);
+  for (uint32_t i = 0; i < L; ++i) {
+    const uint64_t q = from->limbs[i].q;
+    uint64_t h = 1 % q;
+    for (uint32_t k = 0; k < L; ++k)
+      if (k != i) h = hp_mulmod(h, from->limbs[k].q % q, q);
+    const uint64_t hinv = hp_powmod(h, q - 2, q);
+    src[i].m = q;
+    src[i].m2 = 2 * q;
+    src[i].qhatinv = TW{hinv, (uint64_t)(((unsigned __int128)hinv << 64) / q)};
+  }
+  for (uint32_t j = 0; j < K; ++j) {
+    const uint64_t p = to->limbs[j].q;
+    dst[j].m = p;
+    dst[j].m2 = 2 * p;
+    dst[j].qhatinv = TW{0, 0};
+    for (uint32_t i = 0; i < L; ++i) {
+      uint64_t h = 1 % p;
+      for (uint32_t k = 0; k < L; ++k)
+        if (k != i) h = hp_mulmod(h, from->limbs[k].q % p, p);
+      qp[(size_t)j * L + i] = TW{h, (uint64_t)(((unsigned __int128)h << 64) / p)};
+    }
+  }
+  rnt_bconv_s* c = new (std::nothrow) rnt_bconv_s;
+  if (!c) return RNT_E_OOM;
+  c->device = from->device;
+  c->logn = from->logn;
+  c->L = L;
+  c->K = K;
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->d_src, sizeof(BcMod) * L)) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_dst, sizeof(BcMod) * K)) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_qhat_p, sizeof(TW) * qp.size())) != cudaSuccess ||
+      (e = cudaMemcpy(c->d_src, src.data(), sizeof(BcMod) * L, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(c->d_dst, dst.data(), sizeof(BcMod) * K, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(c->d_qhat_p, qp.data(), sizeof(TW) * qp.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    rnt_bconv_destroy(c);
+    return cuda_fail(e);
+  }
+  *out = c;
+  return RNT_OK;
+}
+
+rnt_status rnt_bconv_destroy(rnt_bconv c) {
+  if (!c) return RNT_OK;
+  cudaFree(c->d_src);
+  cudaFree(c->d_dst);
+  cudaFree(c->d_qhat_p);
+  delete c;
+  return RNT_OK;
+}
+
+rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {
+  if (!c) return RNT_E_INVALID_ARG;
+  if (batch == 0) return RNT_OK;
+  if (!out || !in || out == in || !aligned16(out) || !aligned16(in)) return RNT_E_INVALID_ARG;
+  int d = -1;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (d != c->device) return RNT_E_PLAN_MISMATCH;
+  const size_t smem = (size_t)c->L * kBcTile * 8;
+  static size_t attr = 0;  // benign race: idempotent attribute call
+  if (smem > 48 * 1024 && attr < smem) {
+    RNT_CUDA(cudaFuncSetAttribute(k_bconv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const uint32_t n = 1u << c->logn;
+  dim3 grid((n + kBcTile - 1) / kBcTile, batch);
+  k_bconv<<<grid, kBcTile, smem, (cudaStream_t)stream>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in),
+                                                         c->d_src, c->d_dst, c->d_qhat_p, c->L, c->K, c->logn);
   return after_launch();
 }
 

@@ -415,3 +415,40 @@ def test_external_product(logn, n_slot, bg, l):
                 G[t * l + j, t] = O.ntt_fwd(row, q, pi)
         R.external_product(p, d, to_dev(c), to_dev(G), bg, l)
         assert np.array_equal(from_dev(d), c)
+
+
+@pytest.mark.parametrize("logn,L,K,batch", [(16, 12, 13, 1), (10, 5, 4, 7), (4, 3, 2, 5), (12, 45, 3, 2)])
+def test_bconv(logn, L, K, batch):
+    """rnt_bconv_apply bit-exact against the oracle's BConv."""
+    qs = O.primes(logn, L + K)
+    src, dst = qs[:L], qs[L:]
+    ps = R.Plan(logn, src)
+    pd = R.Plan(logn, dst)
+    bc = R.BConv(ps, pd)
+    x = inputs.residues(41, batch, src, 1 << logn)
+    out = empty_dev((batch, K, 1 << logn))
+    bc(out, to_dev(x))
+    got = from_dev(out)
+    for b in range(batch):
+        assert np.array_equal(got[b], O.bconv(x[b], src, dst))
+
+
+def test_modup_pipeline_intt_bconv_ntt():
+    """CKKS ModUp: NTT-form limbs over Q -> INTT -> BConv -> NTT over P,
+    composed from the library calls, against the oracle composition."""
+    logn, L, K = 16, 4, 3
+    qs = O.primes(logn, L + K)
+    src, dst = qs[:L], qs[L:]
+    psi_s = [O.min_psi(q, logn) for q in src]
+    psi_d = [O.min_psi(q, logn) for q in dst]
+    ps, pd = R.Plan(logn, src), R.Plan(logn, dst)
+    bc = R.BConv(ps, pd)
+    A = inputs.residues(42, 1, src, 1 << logn)              # evaluation form over Q
+    coeff = empty_dev(A.shape)
+    R.ntt_inverse(ps, coeff, to_dev(A))
+    ext = empty_dev((1, K, 1 << logn))
+    bc(ext, coeff)
+    R.ntt_forward(pd, ext, ext)
+    want_c = O.batch(O.OP_INV, A, src, psi_s)
+    want = O.batch(O.OP_FWD, O.bconv(want_c[0], src, dst)[None], dst, psi_d)
+    assert np.array_equal(from_dev(ext), want)
