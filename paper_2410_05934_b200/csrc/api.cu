@@ -431,7 +431,7 @@ template <int LOGN>
 static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                  DigitSpec ds, cudaStream_t st) {
   static bool attr_set = false;  // benign race: idempotent attribute call
-  const size_t smem = (size_t)2 * 3 * kWarpBuf * 8;
+  const size_t smem = (size_t)2 * kWarpBuf * 8;
   if (!attr_set) {
     RNT_CUDA(cudaFuncSetAttribute(k_extprod<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;

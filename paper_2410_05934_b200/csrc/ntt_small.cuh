@@ -564,10 +564,12 @@ __device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, co
   __syncwarp();
 }
 
-// last forward pass: CT stages, then acc_i += x (.) z_i (i = 0, 1), kept in [0, 2q)
+// last forward pass: CT stages, then acc_i (+)= x (.) z_i (i = 0, 1), kept in
+// [0, 2q).  The accumulators live in the output pair itself (NTT domain; L2-
+// resident while the slot is in flight), so a warp needs one shared buffer.
 template <int LOGN, int S, int K>
-__device__ __forceinline__ void fwd_pass_mac(u64* buf, u64* acc0, u64* acc1, const u64* z0, const u64* z1, int lane,
-                                             const TW* T, u64 q, u64 q2, u64 qinv) {
+__device__ __forceinline__ void fwd_pass_mac(u64* buf, GView acc0v, GView acc1v, const u64* z0, const u64* z1,
+                                             bool first, int lane, const TW* T, u64 q, u64 q2, u64 qinv) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
 #pragma unroll 1
@@ -579,19 +581,24 @@ __device__ __forceinline__ void fwd_pass_mac(u64* buf, u64* acc0, u64* acc1, con
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     ct_group<S, K>(x, T, g.hi, q, q2);
+    if (acc0v.live(g.poly)) {
+      u64* a0 = const_cast<u64*>(acc0v.at(g.poly)) + jj0;
+      u64* a1 = const_cast<u64*>(acc1v.at(g.poly)) + jj0;
 #pragma unroll
-    for (int i = 0; i < (1 << K); ++i) {
-      const int o = pb + pad_off<LOGN, S, Geo::LO>(i);
-      const int e = jj0 + i * Geo::LO;
-      acc0[o] = csub(acc0[o] + mont_mul(x[i], __ldg(z0 + e), q, qinv), q2);
-      acc1[o] = csub(acc1[o] + mont_mul(x[i], __ldg(z1 + e), q, qinv), q2);
+      for (int i = 0; i < (1 << K); ++i) {
+        const int e = jj0 + i * Geo::LO;
+        const u64 m0 = mont_mul(x[i], __ldg(z0 + e), q, qinv);
+        const u64 m1 = mont_mul(x[i], __ldg(z1 + e), q, qinv);
+        a0[i * Geo::LO] = first ? m0 : csub(a0[i * Geo::LO] + m0, q2);
+        a1[i * Geo::LO] = first ? m1 : csub(a1[i * Geo::LO] + m1, q2);
+      }
     }
   }
   __syncwarp();
 }
 
 template <int LOGN, int KM = 3>
-__global__ void __launch_bounds__(2 * 32, 8)
+__global__ void __launch_bounds__(2 * 32, 12)
 k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restrict__ zhat,
           const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
           uint32_t n_slot, DigitSpec ds) {
@@ -605,15 +612,10 @@ k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restric
   const int lane = threadIdx.x & 31;
   const uint64_t s0 = ((uint64_t)blockIdx.x * 2 + warp) * P;
   if (s0 >= n_slot) return;
-  u64* buf = smem + (size_t)warp * 3 * kWarpBuf;
-  u64* acc0 = buf + kWarpBuf;
-  u64* acc1 = acc0 + kWarpBuf;
-  for (int i = lane; i < kWarpBuf; i += 32) {
-    acc0[i] = 0;
-    acc1[i] = 0;
-  }
-  __syncwarp();
+  u64* buf = smem + (size_t)warp * kWarpBuf;
   const u64 q = lc[0].q, q2 = lc[0].q2, qinv = lc[0].qinv;
+  const GView o0{out, s0, 2ull * N, n_slot};
+  const GView o1{out + N, s0, 2ull * N, n_slot};
   for (uint32_t t = 0; t < 2; ++t) {
     const GView cv{c + (uint64_t)t * N, s0, 2ull * N, n_slot};
     for (uint32_t j = 0; j < ds.levels; ++j) {
@@ -623,19 +625,13 @@ k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restric
         constexpr int p = decltype(P_)::value;
         fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf>(buf, cv, cv, lane, tw_fwd, q, q2);
       });
-      fwd_pass_mac<LOGN, PS::s(NP - 1), PS::k(NP - 1)>(buf, acc0, acc1, zhat + (r * 2 + 0) * N, zhat + (r * 2 + 1) * N,
-                                                       lane, tw_fwd, q, q2, qinv);
+      fwd_pass_mac<LOGN, PS::s(NP - 1), PS::k(NP - 1)>(buf, o0, o1, zhat + (r * 2 + 0) * N, zhat + (r * 2 + 1) * N,
+                                                       r == 0, lane, tw_fwd, q, q2, qinv);
     }
   }
-  const TW s0w = lc[0].ninvR, s1w = lc[0].ninvR_w1;
-  for (uint32_t i = 0; i < 2; ++i) {
-    u64* acc = i ? acc1 : acc0;
-    const GView ov{out + (uint64_t)i * N, s0, 2ull * N, n_slot};
-    sfor<0, NP>([&](auto I_) {
-      constexpr int p = NP - 1 - decltype(I_)::value;
-      inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(acc, ov, ov, lane, tw_inv, s0w, s1w, q, q2);
-    });
-  }
+  // INTT of both accumulators in place (N^{-1} 2^64 scale after the Montgomery products)
+  warp_inverse<LOGN, KM>(buf, o0, o0, lane, tw_inv, lc[0].ninvR, lc[0].ninvR_w1, q, q2);
+  warp_inverse<LOGN, KM>(buf, o1, o1, lane, tw_inv, lc[0].ninvR, lc[0].ninvR_w1, q, q2);
 }
 
 template <int LOGN, int MODE, int W = kTeamWarps>
