@@ -404,6 +404,36 @@ __global__ void k_bfly12(u64* out, const u64* in, u64 w, u64 wp, u64 q, long lon
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// V13: Shoup with W'' = floor(w 2^63 / q) < 2^63: the middle partial-product sum
+// cannot overflow 64 bits (y < 2^62), so no carry capture is needed:
+//   mid = y0 p1 + y1 p0 + hi(y0 p0);  Q = 2 y1 p1 + (mid >> 31)  (= floor(y W'' / 2^63))
+__device__ __forceinline__ void bfly_v13(u64& X, u64& Y, u64 w, u64 wpp, u64 q2, u64 nq) {
+  const uint32_t y0 = (uint32_t)Y, y1 = (uint32_t)(Y >> 32), p0 = (uint32_t)wpp, p1 = (uint32_t)(wpp >> 32);
+  const u64 mid = (u64)y0 * p1 + (u64)y1 * p0 + __umulhi(y0, p0);
+  const u64 Q = (((u64)y1 * p1) << 1) + (mid >> 31);
+  const u64 T = Y * w + Q * nq;
+  const u64 x = X >= q2 ? X - q2 : X;
+  X = x + T;
+  Y = x + q2 - T;
+}
+
+template <int V>
+__global__ void k_bfly13(u64* out, const u64* in, u64 w, u64 wpp, u64 q, long long* cyc) {
+  u64 X[4], Y[4];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < 4; ++i) { X[i] = in[gid * 8 + 2 * i]; Y[i] = in[gid * 8 + 2 * i + 1]; }
+  const u64 q2 = 2 * q, nq = 0ull - q;
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bfly_v13(X[i], Y[i], w, wpp, q2, nq);
+  }
+  long long t1 = clock64();
+  for (int i = 0; i < 4; ++i) { out[gid * 8 + 2 * i] = X[i]; out[gid * 8 + 2 * i + 1] = Y[i]; }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 static u64 mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
 
 int main() {
@@ -474,6 +504,29 @@ int main() {
     run(k_bfly<8>, "V8_c_approx");
     run(k_bfly<9>, "V9_c_approx_umulhi");
     run(k_bfly12, "V12_ptx_noaddend_hiword");
+    {
+      const u64 wpp = (u64)(((u128)w << 63) / q);
+      auto k13 = [&](u64* o, const u64* i, u64 ww, u64 /*wp*/, u64 qq, long long* c) {};
+      (void)k13;
+      k_bfly13<0><<<grid, TPB>>>(dout, din, w, wpp, q, cyc);
+      cudaEventRecord(e0);
+      k_bfly13<0><<<grid, TPB>>>(dout, din, w, wpp, q, cyc);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      CK(cudaMemcpy(hc, cyc, grid * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ho, dout, (size_t)nthr * 64, cudaMemcpyDeviceToHost));
+      long long mx = 0; for (int i = 0; i < grid; ++i) if (hc[i] > mx) mx = hc[i];
+      int bad = 0;
+      for (int i = 0; i < NREF; ++i) {
+        int t = i / 4, k = i % 4;
+        u64 X = ho[t * 8 + 2 * k] % q, Y = ho[t * 8 + 2 * k + 1] % q;
+        u64 rX = h[t * 8 + 2 * k], rY = h[t * 8 + 2 * k + 1];
+        for (int it = 0; it < ITERS; ++it) { u64 tt = mulmod(rY, w, q); u64 nx = (rX + tt) % q, ny = (rX + q - tt) % q; rX = nx; rY = ny; }
+        if (X != rX || Y != rY) ++bad;
+      }
+      if (rep) printf("{\"variant\":\"V13_half_scale_shoup\",\"bfly_per_clk_per_sm\":%.3f,\"ms\":%.4f,\"bad\":%d}\n", 256.0 * 4 * TPB * CPS / mx, ms, bad);
+    }
   }
   {
     // hybrid variant
