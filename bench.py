@@ -320,10 +320,18 @@ def bench_ours(args, wl, parts):
             if ev is not None:
                 ev[i][1].record(stream)
 
+    # end to end: each part on its own user stream (independent batches overlap
+    # their PCIe traffic); the library pipelines chunks inside each call.
+    part_streams = [torch.cuda.Stream() for _ in states]
+
     def step_host():
-        for s in states:
-            R.execute_host(s["plan"], R.OP_POLYMUL_EVAL, s["hc"], s["ha"], s["ws"], b_dev=s["b"],
-                           stream=stream)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        for s, ps in zip(states, part_streams):
+            ps.wait_event(ev)
+            R.execute_host(s["plan"], R.OP_POLYMUL_EVAL, s["hc"], s["ha"], s["ws"], b_dev=s["b"], stream=ps)
+        for ps in part_streams:
+            stream.wait_stream(ps)
 
     def barrier():
         torch.cuda.synchronize()

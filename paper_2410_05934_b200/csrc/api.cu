@@ -34,7 +34,8 @@ struct rnt_plan_s {
   TW* d_rowtw = nullptr;    // n >= 11: natural per-row forward table [L][2^{n1}][2^{n2}] (k_rows)
   // rnt_execute_host pipelining: auxiliary streams, created on first use
   std::mutex aux_mu;
-  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};   // H2D copy, compute, D2H copy
+  std::vector<cudaEvent_t> ev_pool;                    // per-chunk events, reused under aux_mu
   bool is_view = false;     // limb-window view used internally (owns nothing)
 };
 
@@ -566,6 +567,7 @@ rnt_status rnt_plan_destroy(rnt_plan p) {
   cudaFree(p->d_rowtw);
   for (auto& a : p->aux)
     if (a) cudaStreamDestroy(a);
+  for (auto e : p->ev_pool) cudaEventDestroy(e);
   cudaSetDevice(prev);
   delete p;
   return RNT_OK;
@@ -801,7 +803,11 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   // Chunking: ~8 MiB chunks over polynomials (batch > 1) or limbs (batch == 1),
   // round-robin over three internal streams so H2D copy, kernels and D2H copy
   // of successive chunks overlap.  Fork/join with the caller's stream by events.
-  const size_t target = (size_t)8 << 20;
+  static size_t target = 0;  // chunk bytes (tuning knob RNT_CHUNK_MB, default 16 MiB, measured best)
+  if (!target) {
+    const char* ev = getenv("RNT_CHUNK_MB");
+    target = (size_t)(ev && atoi(ev) > 0 ? atoi(ev) : 16) << 20;
+  }
   size_t per_chunk_units = target / unit_bytes;
   if (per_chunk_units < 1) per_chunk_units = 1;
   uint32_t nchunks;
@@ -819,20 +825,22 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
     RNT_CUDA(cudaMemcpyAsync(out_host, dev_ws, total_units * unit_bytes, cudaMemcpyDeviceToHost, st));
     return RNT_OK;
   }
-  {
-    std::lock_guard<std::mutex> g(p->aux_mu);
-    for (auto& a : p->aux)
-      if (!a) RNT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  // Three-stage pipeline: aux[0] copies chunks in, aux[1] runs the kernels of
+  // chunk c once its copy landed, aux[2] copies chunk c out once computed.
+  // Chunks own disjoint parts of dev_ws, so the stages only wait on per-chunk
+  // events and both copy engines stay busy.
+  std::lock_guard<std::mutex> g(p->aux_mu);
+  for (auto& a : p->aux)
+    if (!a) RNT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  while (p->ev_pool.size() < 2 * (size_t)nchunks + 4) {
+    cudaEvent_t e;
+    RNT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->ev_pool.push_back(e);
   }
-  cudaEvent_t fork, join[3];
-  RNT_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  cudaEvent_t fork = p->ev_pool[0];
   RNT_CUDA(cudaEventRecord(fork, st));
-  for (int i = 0; i < 3; ++i) {
-    RNT_CUDA(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
-    RNT_CUDA(cudaStreamWaitEvent(p->aux[i], fork, 0));
-  }
+  for (int i = 0; i < 3; ++i) RNT_CUDA(cudaStreamWaitEvent(p->aux[i], fork, 0));
   for (uint32_t c = 0; c < nchunks && s == RNT_OK; ++c) {
-    cudaStream_t a = p->aux[c % 3];
     size_t u0, nu;
     const uint64_t* bchunk = b_dev;
     rnt_plan_s view;
@@ -857,20 +865,25 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
       nu = nl;
       if (bop) bchunk = b_dev + (size_t)l0 * n;
     }
-    cudaError_t e = cudaMemcpyAsync(dev_ws + u0 * n, in_host + u0 * n, nu * unit_bytes, cudaMemcpyHostToDevice, a);
+    cudaEvent_t ev_in = p->ev_pool[4 + 2 * c], ev_done = p->ev_pool[5 + 2 * c];
+    cudaError_t e = cudaMemcpyAsync(dev_ws + u0 * n, in_host + u0 * n, nu * unit_bytes, cudaMemcpyHostToDevice,
+                                    p->aux[0]);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in, p->aux[0]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->aux[1], ev_in, 0);
     if (e != cudaSuccess) { s = cuda_fail(e); break; }
     s = run_op(const_cast<rnt_plan_s*>(pp), (int)op, dev_ws + u0 * n, dev_ws + u0 * n, bchunk,
-               b_broadcast ? 1 : 0, cb, a);
+               b_broadcast ? 1 : 0, cb, p->aux[1]);
     if (s != RNT_OK) break;
-    e = cudaMemcpyAsync(out_host + u0 * n, dev_ws + u0 * n, nu * unit_bytes, cudaMemcpyDeviceToHost, a);
+    e = cudaEventRecord(ev_done, p->aux[1]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->aux[2], ev_done, 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out_host + u0 * n, dev_ws + u0 * n, nu * unit_bytes, cudaMemcpyDeviceToHost, p->aux[2]);
     if (e != cudaSuccess) { s = cuda_fail(e); break; }
   }
   for (int i = 0; i < 3; ++i) {
-    cudaEventRecord(join[i], p->aux[i]);
-    cudaStreamWaitEvent(st, join[i], 0);
-    cudaEventDestroy(join[i]);
+    cudaEventRecord(p->ev_pool[1 + i], p->aux[i]);
+    cudaStreamWaitEvent(st, p->ev_pool[1 + i], 0);
   }
-  cudaEventDestroy(fork);
   return s;
 }
 
