@@ -312,13 +312,25 @@ def bench_ours(args, wl, parts):
     dom = int(np.argmax(work)) if work else 0
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
-    def step(ev=None):
+    run_streams = [torch.cuda.Stream() for _ in states] if args.concurrent_parts else [stream for _ in states]
+
+    def step(ev=None, span=None):
+        if span is not None:
+            span[0].record(stream)
         for i, s in enumerate(states):
+            rs = run_streams[i]
+            if rs is not stream:
+                rs.wait_stream(stream)
             if ev is not None:
-                ev[i][0].record(stream)
-            R.polymul(s["plan"], s["c"], s["a"], s["b"], b_is_eval=True, stream=stream)
+                ev[i][0].record(rs)
+            R.polymul(s["plan"], s["c"], s["a"], s["b"], b_is_eval=True, stream=rs)
             if ev is not None:
-                ev[i][1].record(stream)
+                ev[i][1].record(rs)
+        for rs in run_streams:
+            if rs is not stream:
+                stream.wait_stream(rs)
+        if span is not None:
+            span[1].record(stream)
 
     # end to end: each part on its own user stream (independent batches overlap
     # their PCIe traffic); the library pipelines chunks inside each call.
@@ -345,16 +357,17 @@ def bench_ours(args, wl, parts):
 
     # ---- device-resident timed region
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in states] for _ in range(args.steps)]
+    spans = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     launches0 = R.launch_count()
     with ClockSampler(local) as clk:
         barrier()
         for k in range(args.steps):
             flush.zero_()   # L2 flush outside the timed events
-            step(evs[k])
+            step(evs[k], spans[k])
         barrier()
     launches = R.launch_count() - launches0
     part_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps)] for i in range(len(states))]
-    step_ms = [sum(part_ms[i][k] for i in range(len(states))) for k in range(args.steps)]
+    step_ms = [spans[k][0].elapsed_time(spans[k][1]) for k in range(args.steps)]
     total_ms = sum(step_ms)
 
     # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
@@ -668,6 +681,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--concurrent-parts", action="store_true",
+                    help="run the independent parts of a step on separate streams")
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
     ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
     ap.add_argument("--extprod", action="store_true", help="SURVEY f1 TFHE external product mode")
