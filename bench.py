@@ -371,17 +371,19 @@ def bench_ours(args, wl, parts):
     total_ms = sum(step_ms)
 
     # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
-    for _ in range(max(1, args.warmup // 2)):
-        step_host()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for k in range(args.steps):
-        step_host()
-    e1.record(stream)
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = float("nan")
+    if args.e2e:
+        for _ in range(max(1, args.warmup // 2)):
+            step_host()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for k in range(args.steps):
+            step_host()
+        e1.record(stream)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
     h2d = sum(s["a"].numel() * 8 for s in states)
 
     # ---- max over ranks
@@ -681,6 +683,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
     ap.add_argument("--concurrent-parts", action="store_true",
                     help="run the independent parts of a step on separate streams")
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
