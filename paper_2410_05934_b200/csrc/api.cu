@@ -36,6 +36,10 @@ struct rnt_plan_s {
   std::mutex aux_mu;
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};   // H2D copy, compute, D2H copy
   std::vector<cudaEvent_t> ev_pool;                    // per-chunk events, reused under aux_mu
+  // limb-window split of single-polynomial multi-limb jobs (N >= 2^11)
+  std::mutex split_mu;
+  cudaStream_t split[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t split_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool is_view = false;     // limb-window view used internally (owns nothing)
 };
 
@@ -568,6 +572,10 @@ rnt_status rnt_plan_destroy(rnt_plan p) {
   for (auto& a : p->aux)
     if (a) cudaStreamDestroy(a);
   for (auto e : p->ev_pool) cudaEventDestroy(e);
+  for (auto& a : p->split)
+    if (a) cudaStreamDestroy(a);
+  for (auto& e : p->split_ev)
+    if (e) cudaEventDestroy(e);
   cudaSetDevice(prev);
   delete p;
   return RNT_OK;
@@ -583,24 +591,12 @@ rnt_status rnt_plan_query(rnt_plan p, uint32_t* log2n, uint32_t* n_limbs, uint64
   return RNT_OK;
 }
 
-static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_, const uint64_t* b_, int bcast,
-                         uint32_t batch, cudaStream_t st) {
-  u64* out = reinterpret_cast<u64*>(out_);
-  const u64* in = reinterpret_cast<const u64*>(in_);
-  const u64* b = reinterpret_cast<const u64*>(b_);
-  const uint64_t units = (uint64_t)batch * p->L;
-  if (p->logn <= 10) {
-    switch (op) {
-      case 0: return warp_dispatch<0>(p, out, in, nullptr, 0, batch, st);
-      case 1: return warp_dispatch<1>(p, out, in, nullptr, 0, batch, st);
-      case 2: return warp_dispatch<2>(p, out, in, b, bcast, batch, st);
-      case 3: return warp_dispatch<3>(p, out, in, b, bcast, batch, st);
-    }
-    return RNT_E_INVALID_ARG;
-  }
+// N >= 2^11: op 3 computes NTT(b) into a stream-ordered temporary, then runs
+// the fused eval-form path; ops 0..2 go straight to the kernel chain.
+static rnt_status run_large(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* b, int bcast,
+                            uint32_t batch, cudaStream_t st) {
   if (op == 3) {
-    // NTT(b) into a stream-ordered temporary, then the fused eval-form path.
-    const uint64_t bunits = bcast ? p->L : units;
+    const uint64_t bunits = (uint64_t)(bcast ? 1u : batch) * p->L;
     const size_t bytes = (size_t)bunits << (p->logn + 3);
     u64* tmp = nullptr;
     RNT_CUDA(cudaMallocAsync(&tmp, bytes, st));
@@ -611,6 +607,57 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
     return s;
   }
   return large_dispatch(p, op, out, in, b, bcast, batch, st);
+}
+
+static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_, const uint64_t* b_, int bcast,
+                         uint32_t batch, cudaStream_t st) {
+  u64* out = reinterpret_cast<u64*>(out_);
+  const u64* in = reinterpret_cast<const u64*>(in_);
+  const u64* b = reinterpret_cast<const u64*>(b_);
+  if (p->logn <= 10) {
+    switch (op) {
+      case 0: return warp_dispatch<0>(p, out, in, nullptr, 0, batch, st);
+      case 1: return warp_dispatch<1>(p, out, in, nullptr, 0, batch, st);
+      case 2: return warp_dispatch<2>(p, out, in, b, bcast, batch, st);
+      case 3: return warp_dispatch<3>(p, out, in, b, bcast, batch, st);
+    }
+    return RNT_E_INVALID_ARG;
+  }
+  // A single polynomial with many limbs (cfg3) launches few CTAs per kernel and
+  // pays each kernel's ramp and tail three times; running G limb windows as
+  // independent kernel chains on G streams lets the windows overlap
+  // (measured: 2^16 x 45 limbs polymul 0.103 -> 0.094 ms with G = 2).
+  static int split_g = -1;
+  if (split_g < 0) {
+    const char* ev = getenv("RNT_SPLIT");
+    split_g = ev ? atoi(ev) : 2;
+    if (split_g > 4) split_g = 4;
+  }
+  if (split_g > 1 && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
+    std::lock_guard<std::mutex> g(p->split_mu);
+    for (int i = 0; i < split_g; ++i)
+      if (!p->split[i]) RNT_CUDA(cudaStreamCreateWithFlags(&p->split[i], cudaStreamNonBlocking));
+    for (int i = 0; i <= split_g; ++i)
+      if (!p->split_ev[i]) RNT_CUDA(cudaEventCreateWithFlags(&p->split_ev[i], cudaEventDisableTiming));
+    RNT_CUDA(cudaEventRecord(p->split_ev[split_g], st));
+    const size_t n = (size_t)1 << p->logn;
+    const uint32_t per = (p->L + split_g - 1) / split_g;
+    rnt_status s = RNT_OK;
+    for (int gi = 0; gi < split_g; ++gi) {
+      const uint32_t l0 = gi * per;
+      const uint32_t nl = p->L - l0 < per ? p->L - l0 : per;
+      rnt_plan_s view;
+      make_view(p, l0, nl, &view);
+      RNT_CUDA(cudaStreamWaitEvent(p->split[gi], p->split_ev[split_g], 0));
+      if (s == RNT_OK)
+        s = run_large(&view, op, out + l0 * n, in + l0 * n, b ? b + l0 * n : nullptr, bcast, 1, p->split[gi]);
+      // Always join, so `st` never runs ahead of work already queued.
+      RNT_CUDA(cudaEventRecord(p->split_ev[gi], p->split[gi]));
+      RNT_CUDA(cudaStreamWaitEvent(st, p->split_ev[gi], 0));
+    }
+    return s;
+  }
+  return run_large(p, op, out, in, b, bcast, batch, st);
 }
 
 rnt_status rnt_ntt_forward(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {

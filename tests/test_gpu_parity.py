@@ -309,13 +309,43 @@ def test_execute_host_chunked_pipeline(logn, limbs, batch, op):
     assert np.array_equal(hout.numpy().view(np.uint64), want)
 
 
+@pytest.mark.parametrize("logn,limbs", [(11, 4), (12, 5), (14, 7), (16, 45)])
+@pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul", "polymul_bcast"])
+def test_limb_split_single_poly(logn, limbs, op):
+    """batch == 1 with many limbs runs as limb windows on internal streams
+    (run_op split); odd limb counts give a ragged last window."""
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    n = 1 << logn
+    a = inputs.residues(21, 1, ps, n)
+    b = inputs.residues(22, 1, ps, n)
+    d = empty_dev(a.shape)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        if op == "fwd":
+            R.ntt_forward(p, d, to_dev(a), stream=s)
+            want = O.batch(O.OP_FWD, a, ps, psi, n_threads=8)
+        elif op == "inv":
+            R.ntt_inverse(p, d, to_dev(a), stream=s)
+            want = O.batch(O.OP_INV, a, ps, psi, n_threads=8)
+        elif op == "polymul_eval":
+            bh = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+            R.polymul(p, d, to_dev(a), to_dev(bh), b_is_eval=True, stream=s)
+            want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8)
+        else:
+            R.polymul(p, d, to_dev(a), to_dev(b), b_broadcast=(op == "polymul_bcast"), stream=s)
+            want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8)
+    s.synchronize()
+    assert np.array_equal(from_dev(d), want)
+
+
 VARIANT_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
 import inputs, oracle as O, paper_2410_05934_b200 as R
 from helpers import params, to_dev, from_dev, empty_dev
 ok = True
-for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3)):
+for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3), (16, 9, 1), (12, 8, 1)):
     ps, psi = params(logn, limbs)
     p = R.Plan(logn, ps)
     a = inputs.residues(3, batch, ps, 1 << logn); b = inputs.residues(4, batch, ps, 1 << logn)
@@ -325,12 +355,15 @@ for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3)):
     R.ntt_inverse(p, d, to_dev(bh)); ok &= np.array_equal(from_dev(d), b)
     R.polymul(p, d, to_dev(a), to_dev(bh), b_is_eval=True)
     ok &= np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bh))
+    R.polymul(p, d, to_dev(a), to_dev(b[:1]), b_broadcast=True)
+    ok &= np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL, a, ps, psi, b=b[:1], b_broadcast=True))
 print("VARIANT_OK" if ok else "VARIANT_BAD")
 """
 
 
 @pytest.mark.parametrize("env", [{"RNT_SMALL_VARIANT": str(v)} for v in (1, 4, 5, 6, 7, 8, 11, 13)] +
-                         [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)])
+                         [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)] +
+                         [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
