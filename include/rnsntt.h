@@ -51,6 +51,14 @@ typedef enum {
   RNT_E_OOM = 7            /* device or host allocation failed */
 } rnt_status;
 
+/* Residue precondition (reading C6): every input residue of limb l must be
+ * canonical, 0 <= r < q_l.  The hot path does not check it (a violation gives
+ * undefined output).  With the environment variable RNT_DEBUG=1 set when the
+ * library first runs an operation, rnt_ntt_forward / rnt_ntt_inverse /
+ * rnt_pointwise_mul / rnt_polymul / rnt_automorph validate their inputs on
+ * the device first, synchronise `stream`, and return RNT_E_INVALID_ARG (no
+ * output written) if any residue is out of range. */
+
 #define RNT_MIN_LOG2N 4u
 #define RNT_MAX_LOG2N 16u
 #define RNT_MAX_LIMBS 1024u

@@ -69,6 +69,7 @@ def _load():
                 "or_decompose": (None, [_u64p, u64, u64, u32, u32]),
                 "or_external_product": (None, [_u64p, _u64p, _u64p, u32, u64, u64, u32, u32]),
                 "or_bconv": (None, [_u64p, _u64p, u64, _u64p, u32, _u64p, u32]),
+                "or_keyswitch": (None, [_u64p, _u64p, _u64p, _u64p, u32, _u64p, u32, _u64p, u32, u32]),
                 "or_batch": (i32, [i32, _u64p, _u64p, i32, u32, u32, u32, _u64p, _u64p, i32]),
             }
             for name, (res, args) in sig.items():
@@ -237,6 +238,31 @@ def bconv(x, q_basis, p_basis) -> np.ndarray:
         _check_canonical(x[i], int(qs[i]))
     out = np.zeros((ps.size, n), dtype=np.uint64)
     _load().or_bconv(_p(out), _p(x), n, _p(qs), L, _p(ps), ps.size)
+    return out
+
+
+def keyswitch(d, evk, q_basis, p_basis, dnum: int, add0=None) -> np.ndarray:
+    """CKKS hybrid key switching (f2; readings KS1-KS4):
+    d [L][N] and evk [dnum][2][L+K][N] in NTT form -> out [2][L][N] NTT form over Q."""
+    d = np.ascontiguousarray(d, dtype=np.uint64)
+    L, n = d.shape
+    qs, ps = _vec(q_basis), _vec(p_basis)
+    K = ps.size
+    assert qs.size == L and 1 <= dnum <= L
+    alpha = -(-L // dnum)
+    if (dnum - 1) * alpha >= L:
+        raise ValueError("empty digit: (dnum - 1) * ceil(L / dnum) >= L")
+    z = np.ascontiguousarray(evk, dtype=np.uint64)
+    assert z.shape == (dnum, 2, L + K, n)
+    for i in range(L):
+        _check_canonical(d[i], int(qs[i]))
+    a0 = None
+    if add0 is not None:
+        a0 = np.ascontiguousarray(add0, dtype=np.uint64)
+        assert a0.shape == (L, n)
+    out = np.zeros((2, L, n), dtype=np.uint64)
+    _load().or_keyswitch(_p(out), _p(d), _p(z), _p(a0) if a0 is not None else None, n.bit_length() - 1,
+                         _p(qs), L, _p(ps), K, dnum)
     return out
 
 

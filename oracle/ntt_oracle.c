@@ -348,6 +348,82 @@ void or_bconv(uint64_t* out, const uint64_t* in, uint64_t n, const uint64_t* q, 
   free(qhat_inv); free(qhat_p); free(y);
 }
 
+/* CKKS hybrid key switching ("critical key switching ... NTT,
+ * BConv, ModMul, ModAdd, Automorph"; parameters (N, L, dnum) of
+ * P:831).  The paper gives no algorithm text; readings KS1-KS4
+ * fix the standard hybrid method, which this function follows step by step:
+ *   Q = {q_0..q_{L-1}}, P = {p_0..p_{K-1}}, extended basis QP = Q then P.
+ *   digits (KS2): alpha = ceil(L / dnum); digit j = limbs [j alpha, min(L, (j+1) alpha)).
+ *   1. x = INTT_Q(d)                                  (d in NTT form over Q)
+ *   2. for each digit j: ModUp  e_j[t] = BConv_{D_j -> t}(x[D_j]) for t not in D_j,
+ *                               e_j[t] = x[t] for t in D_j;  then NTT_t(e_j[t])
+ *   3. u_k[t] = sum_j e_j[t] * evk[j][k][t]  (k = 0, 1; NTT form over QP)
+ *   4. ModDown (KS3): w = BConv_{P -> Q}(INTT_P(u_k[P])), NTT_Q(w),
+ *                     out_k[i] = (u_k[i] - w[i]) * P^{-1} mod q_i   (+ add0 for k = 0)
+ * psi of every prime: reading C1 (or_min_psi).  evk: [dnum][2][L+K][N], out: [2][L][N],
+ * add0: [L][N] or NULL.  All in NTT form (bit-reversed order, reading C3). */
+void or_keyswitch(uint64_t* out, const uint64_t* d, const uint64_t* evk, const uint64_t* add0, uint32_t logn,
+                  const uint64_t* q, uint32_t L, const uint64_t* p, uint32_t K, uint32_t dnum) {
+  const uint64_t n = (uint64_t)1 << logn;
+  const uint32_t LK = L + K, alpha = (L + dnum - 1) / dnum;
+  uint64_t* mod = (uint64_t*)malloc(LK * sizeof(uint64_t));
+  for (uint32_t t = 0; t < L; ++t) mod[t] = q[t];
+  for (uint32_t t = 0; t < K; ++t) mod[L + t] = p[t];
+  uint64_t* fwd = (uint64_t*)malloc((size_t)LK * n * sizeof(uint64_t));
+  uint64_t* inv = (uint64_t*)malloc((size_t)LK * n * sizeof(uint64_t));
+  uint64_t* ninv = (uint64_t*)malloc(LK * sizeof(uint64_t));
+  for (uint32_t t = 0; t < LK; ++t)
+    or_tables(mod[t], or_min_psi(mod[t], logn), logn, fwd + (size_t)t * n, inv + (size_t)t * n, ninv + t);
+  /* 1. coefficient form of d */
+  uint64_t* x = (uint64_t*)malloc((size_t)L * n * sizeof(uint64_t));
+  memcpy(x, d, (size_t)L * n * sizeof(uint64_t));
+  for (uint32_t t = 0; t < L; ++t) or_ntt_inv(x + (size_t)t * n, logn, q[t], inv + (size_t)t * n, ninv[t]);
+  /* 2-3. ModUp each digit, NTT, multiply-accumulate with the key */
+  uint64_t* u = (uint64_t*)calloc((size_t)2 * LK * n, sizeof(uint64_t));
+  uint64_t* e = (uint64_t*)malloc((size_t)LK * n * sizeof(uint64_t));
+  for (uint32_t j = 0; j < dnum; ++j) {
+    const uint32_t lo = j * alpha, hi = (j + 1) * alpha < L ? (j + 1) * alpha : L;
+    for (uint32_t t = 0; t < LK; ++t) {
+      uint64_t* et = e + (size_t)t * n;
+      if (t >= lo && t < hi)
+        memcpy(et, x + (size_t)t * n, n * sizeof(uint64_t));
+      else
+        or_bconv(et, x + (size_t)lo * n, n, q + lo, hi - lo, mod + t, 1);
+      or_ntt_fwd(et, logn, mod[t], fwd + (size_t)t * n);
+      for (uint32_t k = 0; k < 2; ++k) {
+        const uint64_t* key = evk + (((size_t)j * 2 + k) * LK + t) * n;
+        uint64_t* ut = u + ((size_t)k * LK + t) * n;
+        for (uint64_t c = 0; c < n; ++c) ut[c] = or_addmod(ut[c], or_mulmod(et[c], key[c], mod[t]), mod[t]);
+      }
+    }
+  }
+  /* 4. ModDown */
+  uint64_t* pinv = (uint64_t*)malloc(L * sizeof(uint64_t));
+  for (uint32_t i = 0; i < L; ++i) {
+    uint64_t pp = 1 % q[i];
+    for (uint32_t t = 0; t < K; ++t) pp = or_mulmod(pp, p[t] % q[i], q[i]);
+    pinv[i] = or_powmod(pp, q[i] - 2, q[i]);
+  }
+  uint64_t* up = (uint64_t*)malloc((size_t)K * n * sizeof(uint64_t));
+  uint64_t* w = (uint64_t*)malloc((size_t)L * n * sizeof(uint64_t));
+  for (uint32_t k = 0; k < 2; ++k) {
+    memcpy(up, u + ((size_t)k * LK + L) * n, (size_t)K * n * sizeof(uint64_t));
+    for (uint32_t t = 0; t < K; ++t) or_ntt_inv(up + (size_t)t * n, logn, p[t], inv + (size_t)(L + t) * n, ninv[L + t]);
+    or_bconv(w, up, n, p, K, q, L);
+    for (uint32_t i = 0; i < L; ++i) {
+      uint64_t* wi = w + (size_t)i * n;
+      or_ntt_fwd(wi, logn, q[i], fwd + (size_t)i * n);
+      const uint64_t* ui = u + ((size_t)k * LK + i) * n;
+      uint64_t* oi = out + ((size_t)k * L + i) * n;
+      for (uint64_t c = 0; c < n; ++c) {
+        oi[c] = or_mulmod(or_submod(ui[c], wi[c], q[i]), pinv[i], q[i]);
+        if (k == 0 && add0) oi[c] = or_addmod(oi[c], add0[(size_t)i * n + c], q[i]);
+      }
+    }
+  }
+  free(mod); free(fwd); free(inv); free(ninv); free(x); free(u); free(e); free(pinv); free(up); free(w);
+}
+
 /* ---------------------------------------------------------- batch driver */
 /* Layout (reading C10): [batch][n_limbs][N], limb l uses moduli[l], psi[l].
  * op: 0 forward, 1 inverse, 2 polymul-with-eval-operand c = INTT(NTT(a) . b_hat),

@@ -32,6 +32,8 @@ void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_
                          uint64_t psi, uint32_t base_log2, uint32_t levels);
 void or_bconv(uint64_t* out, const uint64_t* in, uint64_t n, const uint64_t* q, uint32_t L, const uint64_t* p,
               uint32_t K);
+void or_keyswitch(uint64_t* out, const uint64_t* d, const uint64_t* evk, const uint64_t* add0, uint32_t logn,
+                  const uint64_t* q, uint32_t L, const uint64_t* p, uint32_t K, uint32_t dnum);
 int or_batch(int op, uint64_t* data, const uint64_t* b, int b_bcast, uint32_t batch,
              uint32_t n_limbs, uint32_t logn, const uint64_t* moduli, const uint64_t* psi,
              int n_threads);

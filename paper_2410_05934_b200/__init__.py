@@ -213,3 +213,10 @@ rnt_external_product = external_product
 rnt_execute_host = execute_host
 rnt_status_string = status_string
 rnt_launch_count = launch_count
+
+
+# Domain-tagged polynomial layer: RnsPoly + mismatch errors.
+from . import poly  # noqa: E402
+from .poly import COEFF, EVAL, BasisMismatch, DomainMismatch, PlanMismatch, RnsPoly  # noqa: E402
+
+__all__ += ["poly", "RnsPoly", "COEFF", "EVAL", "DomainMismatch", "BasisMismatch", "PlanMismatch"]

@@ -172,6 +172,17 @@ k_bconv(u64* __restrict__ out, const u64* __restrict__ in, const BcMod* __restri
   }
 }
 
+// RNT_DEBUG=1: residue range check of the inputs (reading C6).  Sets *bad
+// when some element of limb (u % L) is >= q.
+__global__ void k_check_range(const u64* __restrict__ x, const LimbC* __restrict__ lc, uint32_t L, uint32_t logn,
+                              uint64_t total, int* __restrict__ bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  int any = 0;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride)
+    any |= __ldg(x + e) >= lc[(e >> logn) % L].q;
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 static int g_num_sms = 0;
 static int num_sms() {
   if (!g_num_sms) {
@@ -412,6 +423,37 @@ static rnt_status check_plan_device(const rnt_plan_s* p) {
   cudaError_t e = cudaGetDevice(&d);
   if (e != cudaSuccess) return cuda_fail(e);
   return d == p->device ? RNT_OK : RNT_E_PLAN_MISMATCH;
+}
+
+static int num_sms();
+
+static bool debug_checks() {
+  static int on = -1;
+  if (on < 0) {
+    const char* ev = getenv("RNT_DEBUG");
+    on = ev && atoi(ev) > 0;
+  }
+  return on;
+}
+
+// Debug-only (RNT_DEBUG=1): validate that `batch` polynomials (or, with
+// units_override, that many limb vectors) at x are canonical.  Synchronises st.
+static rnt_status debug_validate(const rnt_plan_s* p, const void* x, uint64_t units, cudaStream_t st) {
+  if (!debug_checks() || !units) return RNT_OK;
+  int* bad = nullptr;
+  RNT_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  RNT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const uint64_t total = units << p->logn;
+  uint64_t blocks = (total + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  k_check_range<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const u64*>(x), p->d_lc, p->L, p->logn, total, bad);
+  int h = 0;
+  RNT_CUDA(cudaGetLastError());
+  RNT_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RNT_CUDA(cudaFreeAsync(bad, st));
+  RNT_CUDA(cudaStreamSynchronize(st));
+  return h ? RNT_E_INVALID_ARG : RNT_OK;
 }
 
 static rnt_status check_data(const rnt_plan_s* p, const void* a, const void* b, uint32_t batch) {
@@ -663,12 +705,14 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
 rnt_status rnt_ntt_forward(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {
   rnt_status s = check_data(p, out, in, batch);
   if (s != RNT_OK || batch == 0) return s;
+  if ((s = debug_validate(p, in, (uint64_t)batch * p->L, (cudaStream_t)stream)) != RNT_OK) return s;
   return run_op(p, 0, out, in, nullptr, 0, batch, (cudaStream_t)stream);
 }
 
 rnt_status rnt_ntt_inverse(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream) {
   rnt_status s = check_data(p, out, in, batch);
   if (s != RNT_OK || batch == 0) return s;
+  if ((s = debug_validate(p, in, (uint64_t)batch * p->L, (cudaStream_t)stream)) != RNT_OK) return s;
   return run_op(p, 1, out, in, nullptr, 0, batch, (cudaStream_t)stream);
 }
 
@@ -677,6 +721,9 @@ rnt_status rnt_pointwise_mul(rnt_plan p, uint64_t* c, const uint64_t* a_hat, con
   rnt_status s = check_data(p, c, a_hat, batch);
   if (s != RNT_OK || batch == 0) return s;
   if (!b_hat || !aligned16(b_hat)) return RNT_E_INVALID_ARG;
+  if ((s = debug_validate(p, a_hat, (uint64_t)batch * p->L, (cudaStream_t)stream)) != RNT_OK ||
+      (s = debug_validate(p, b_hat, (uint64_t)(b_broadcast ? 1u : batch) * p->L, (cudaStream_t)stream)) != RNT_OK)
+    return s;
   const uint64_t total2 = ((uint64_t)batch * p->L << p->logn) / 2;
   const int threads = 256;
   uint64_t blocks = (total2 + threads - 1) / threads;
@@ -694,6 +741,7 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
   if (s != RNT_OK || batch == 0) return s;
   const uint32_t two_n = 2u << p->logn;
   if (out == in || (galois_elt & 1u) == 0 || galois_elt >= two_n) return RNT_E_INVALID_ARG;
+  if ((s = debug_validate(p, in, (uint64_t)batch * p->L, (cudaStream_t)stream)) != RNT_OK) return s;
   uint32_t ginv = 1;  // g^{-1} mod 2N: g^(N/2 - 1), the group (Z/2N)^* has exponent N/2 (N >= 4)
   {
     uint64_t b = galois_elt, e = (two_n / 4) - 1, r = 1;
@@ -831,6 +879,9 @@ rnt_status rnt_polymul(rnt_plan p, uint64_t* c, const uint64_t* a, const uint64_
   rnt_status s = check_data(p, c, a, batch);
   if (s != RNT_OK || batch == 0) return s;
   if (!b || !aligned16(b) || b == c) return RNT_E_INVALID_ARG;
+  if ((s = debug_validate(p, a, (uint64_t)batch * p->L, (cudaStream_t)stream)) != RNT_OK ||
+      (s = debug_validate(p, b, (uint64_t)(b_broadcast ? 1u : batch) * p->L, (cudaStream_t)stream)) != RNT_OK)
+    return s;
   return run_op(p, b_is_eval ? 2 : 3, c, a, b, b_broadcast ? 1 : 0, batch, (cudaStream_t)stream);
 }
 

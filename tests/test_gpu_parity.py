@@ -485,3 +485,44 @@ def test_modup_pipeline_intt_bconv_ntt():
     want_c = O.batch(O.OP_INV, A, src, psi_s)
     want = O.batch(O.OP_FWD, O.bconv(want_c[0], src, dst)[None], dst, psi_d)
     assert np.array_equal(from_dev(ext), want)
+
+
+DEBUG_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import inputs, oracle as O, paper_2410_05934_b200 as R
+from helpers import params, to_dev, from_dev, empty_dev
+res = []
+for logn, limbs, batch in ((10, 2, 3), (16, 2, 1)):
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    a = inputs.residues(5, batch, ps, 1 << logn)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))                      # canonical: accepted, correct
+    res.append(np.array_equal(from_dev(d), O.batch(O.OP_FWD, a, ps, psi)))
+    bad = a.copy(); bad[-1, 1, 7] = ps[1]               # r = q_1 in the last limb vector
+    for call in (lambda: R.ntt_forward(p, d, to_dev(bad)),
+                 lambda: R.ntt_inverse(p, d, to_dev(bad)),
+                 lambda: R.pointwise_mul(p, d, to_dev(a), to_dev(bad)),
+                 lambda: R.polymul(p, d, to_dev(bad), to_dev(a)),
+                 lambda: R.automorph(p, d, to_dev(bad), 3)):
+        try:
+            call(); torch.cuda.synchronize(); res.append(False)
+        except R.RntError as e:
+            res.append(e.code == R.RNT_E_INVALID_ARG)
+print("DEBUG_OK" if all(res) else "DEBUG_BAD %r" % res)
+"""
+
+
+def test_debug_range_validation():
+    """RNT_DEBUG=1: non-canonical residues are rejected with RNT_E_INVALID_ARG
+    (reading C6; include/rnsntt.h), canonical inputs still computed exactly."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = DEBUG_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RNT_DEBUG": "1"}, capture_output=True,
+                       text=True, timeout=600)
+    assert "DEBUG_OK" in r.stdout, r.stdout + r.stderr
