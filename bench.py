@@ -674,6 +674,75 @@ def bench_modup(args):
                       "limb_transforms_per_s": (Lin + Kout) / (ms[0] * 1e-3 + ms[2] * 1e-3)}), flush=True)
 
 
+def bench_keyswitch(args):
+    """CKKS hybrid key switching (rnt_keyswitch_apply) and HROT =
+    automorph(c0), automorph(c1), key switch of sigma(c1) with sigma(c0) added,
+    at the paper's (N, L, dnum) = (2^16, 44 + 1 = 45 limbs, 45) with one
+    special prime (reading KS1), and a dnum = 3 hybrid variant (15 special primes).
+    Context, not a target: the paper's HEROT on A100 is 5.13 ms (tab:ckks-gpu-performance)."""
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    res = {}
+    logn = 16
+    n = 1 << logn
+    for (L, K, dnum) in ((45, 1, 45), (45, 15, 3)):
+        mods = primes_for(logn, L + K)
+        qs = mods[:L]
+        qp, qpp = R.Plan(logn, qs), R.Plan(logn, mods)
+        ks = R.KeySwitch(qp, qpp, dnum)
+        c = torch.from_numpy(inputs.residues(0, 2, qs, n).view(np.int64)).cuda()          # ciphertext (c0, c1)
+        evk = torch.from_numpy(inputs.residues(1, 2 * dnum, mods, n).view(np.int64)).cuda()
+        sc = torch.empty_like(c)
+        out = torch.empty_like(c)
+        g = 5                                                                            # rotation by one slot
+        per = L * n
+
+        def hrot():
+            R.automorph(qp, sc, c, g, ntt_domain=True)
+            ks(out, sc[1], evk, add0=sc[0])
+
+        def kswitch():
+            ks(out, c[1], evk)
+
+        for name, fn in (("keyswitch", kswitch), ("hrot", hrot)):
+            for _ in range(args.warmup):
+                fn()
+            ms = []
+            for _ in range(args.steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            t = statistics.mean(ms)
+            xf = L + dnum * (L + K) + 2 * K + 2 * L
+            bf = xf * (n // 2) * logn
+            res[f"L{L}_K{K}_dnum{dnum}_{name}"] = {
+                "ms": t, "ms_min": min(ms), "ms_p90": sorted(ms)[int(0.9 * (len(ms) - 1))],
+                "limb_transforms": xf, "gbfly_per_s": bf / (t * 1e-3) / 1e9,
+                "frac_alu_transforms_only": bf / (t * 1e-3) / 1e9 / peak_bfly,
+                "evk_GB": evk.numel() * 8 / 1e9,
+                "evk_read_floor_ms": evk.numel() * 8 / (hbm * 1e9) * 1e3}
+        del ks, evk
+        torch.cuda.empty_cache()
+    print(json.dumps({"mode": "keyswitch", "metric": "CKKS hybrid key switch / HROT latency (ms), N=2^16",
+                      "paper_context": {"HEROT_ms_A100_Chameleon": 5.13, "params": "(2^16, logQ 2305, L 44, dnum 45)",
+                                        "cite": "PAPER.md tab:ckks-gpu-performance (P:849-856)"},
+                      "roofline": {"bound": "alu", "peak": peak_bfly, "unit": "Gbutterfly/s"},
+                      "results": res}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -690,6 +759,7 @@ def main():
     ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
     ap.add_argument("--extprod", action="store_true", help="SURVEY f1 TFHE external product mode")
     ap.add_argument("--modup", action="store_true", help="SURVEY f2 CKKS ModUp (INTT -> BConv -> NTT) mode")
+    ap.add_argument("--keyswitch", action="store_true", help="SURVEY f2 CKKS key switch / HROT mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -703,6 +773,8 @@ def main():
         bench_extprod(args)
     elif args.modup:
         bench_modup(args)
+    elif args.keyswitch:
+        bench_keyswitch(args)
     elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:

@@ -150,6 +150,38 @@ rnt_status rnt_bconv_create(rnt_bconv* out, rnt_plan from, rnt_plan to);
 rnt_status rnt_bconv_destroy(rnt_bconv c);
 rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint32_t batch, void* stream);
 
+/* CKKS hybrid key switching: "critical key switching" built
+ * from NTT, BConv, ModMul and ModAdd, at the paper's parameters
+ * (N, L, dnum) = (2^16, 44, 45) or any other.  Readings KS1-KS4
+ * fix the method the paper leaves unstated:
+ *   Q = q_plan's moduli (L limbs); qp_plan's moduli = Q followed by the
+ *   special primes P (K = n_limbs(qp_plan) - L >= 1), same N, same psi on Q.
+ *   Digits: alpha = ceil(L / dnum) primes each, digit j = limbs
+ *   [j alpha, min(L, (j+1) alpha)), every digit non-empty.
+ *   apply:  x = INTT_Q(d);  for each digit j: e_j = ModUp(x[D_j]) over QP
+ *           (BConv from the digit's primes to all other primes of QP),
+ *           NTT_QP(e_j);  u_k = sum_j e_j (.) evk[j][k] (k = 0, 1);
+ *           out_k = (u_k[Q] - NTT_Q(BConv_{P->Q}(INTT_P(u_k[P])))) P^{-1} mod q_i,
+ *           plus add0 on out_0 when add0 != NULL.
+ * d:    device [L][N], NTT form over Q (e.g. c_1 of a ciphertext, after an
+ *       automorphism for a rotation).
+ * evk:  device [dnum][2][L+K][N], NTT form over QP (the switching key rows).
+ * add0: device [L][N] NTT form over Q, or NULL (HROT adds sigma(c_0) here).
+ * out:  device [2][L][N], NTT form over Q; must not overlap the inputs.
+ * The handle borrows both plans (keep them alive) and owns a device workspace
+ * of rnt_keyswitch_query(...workspace_bytes) bytes, allocated at create; one
+ * apply runs at a time per handle (serialised on the host; calls on different
+ * streams are ordered by the caller).  Requires dnum * max(m)^2 < 2^128
+ * (exact 128-bit key inner product).  Errors: RNT_E_INVALID_ARG (plans do not
+ * match, dnum out of range, null/unaligned pointers), RNT_E_PLAN_MISMATCH,
+ * RNT_E_CUDA / RNT_E_OOM. */
+typedef struct rnt_keyswitch_s* rnt_keyswitch;
+rnt_status rnt_keyswitch_create(rnt_keyswitch* out, rnt_plan q_plan, rnt_plan qp_plan, uint32_t dnum);
+rnt_status rnt_keyswitch_destroy(rnt_keyswitch ks);
+rnt_status rnt_keyswitch_query(rnt_keyswitch ks, uint32_t* alpha, uint64_t* workspace_bytes);
+rnt_status rnt_keyswitch_apply(rnt_keyswitch ks, uint64_t* out, const uint64_t* d, const uint64_t* evk,
+                               const uint64_t* add0, void* stream);
+
 /* Operation codes for rnt_execute_host. */
 typedef enum {
   RNT_OP_FORWARD = 0,

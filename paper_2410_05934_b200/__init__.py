@@ -28,7 +28,7 @@ from ._lib import (RNT_E_CUDA, RNT_E_INVALID_ARG, RNT_E_MODULUS, RNT_E_OOM, RNT_
                    status_string)
 
 __all__ = [
-    "Plan", "BConv", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "external_product",
+    "Plan", "BConv", "KeySwitch", "ntt_forward", "ntt_inverse", "pointwise_mul", "polymul", "automorph", "external_product",
     "execute_host",
     "RntError", "status_string", "launch_count", "lib_path",
     "RNT_OK", "RNT_E_INVALID_ARG", "RNT_E_UNSUPPORTED_N", "RNT_E_MODULUS", "RNT_E_ROOT",
@@ -183,6 +183,40 @@ class BConv:
     def destroy(self):
         if getattr(self, "_h", None) is not None:
             _lib.L.rnt_bconv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class KeySwitch:
+    """CKKS hybrid key switching (rnt_keyswitch_*).
+
+    q_plan: basis Q (L limbs); qp_plan: Q followed by the special primes P;
+    dnum digits of ceil(L / dnum) primes.  __call__(out [2][L][N], d [L][N],
+    evk [dnum][2][L+K][N], add0 [L][N] or None), all NTT form.
+    """
+
+    def __init__(self, q_plan: Plan, qp_plan: Plan, dnum: int):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.L.rnt_keyswitch_create(ctypes.byref(h), q_plan.handle, qp_plan.handle, int(dnum)))
+        self._h = h
+        self.q_plan, self.qp_plan, self.dnum = q_plan, qp_plan, int(dnum)
+        a = ctypes.c_uint32()
+        wb = ctypes.c_uint64()
+        _lib.check(_lib.L.rnt_keyswitch_query(h, ctypes.byref(a), ctypes.byref(wb)))
+        self.alpha, self.workspace_bytes = int(a.value), int(wb.value)
+
+    def __call__(self, out, d, evk, add0=None, stream=None) -> None:
+        _lib.check(_lib.L.rnt_keyswitch_apply(self._h, _ptr(out), _ptr(d), _ptr(evk),
+                                              _ptr(add0) if add0 is not None else None, _stream(stream)))
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.L.rnt_keyswitch_destroy(self._h)
             self._h = None
 
     def __del__(self):

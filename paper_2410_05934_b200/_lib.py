@@ -32,6 +32,10 @@ SIGNATURES = {
     "rnt_bconv_create": (_i32, [ctypes.POINTER(_vp), _vp, _vp]),
     "rnt_bconv_destroy": (_i32, [_vp]),
     "rnt_bconv_apply": (_i32, [_vp, _vp, _vp, _u32, _vp]),
+    "rnt_keyswitch_create": (_i32, [ctypes.POINTER(_vp), _vp, _vp, _u32]),
+    "rnt_keyswitch_destroy": (_i32, [_vp]),
+    "rnt_keyswitch_query": (_i32, [_vp, ctypes.POINTER(_u32), _u64p]),
+    "rnt_keyswitch_apply": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "rnt_execute_host": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _u32, _i32, _vp]),
     "rnt_status_string": (ctypes.c_char_p, [_i32]),
     "rnt_last_cuda_error": (_i32, []),

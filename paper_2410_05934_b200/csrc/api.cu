@@ -18,6 +18,7 @@
 #include "modarith.cuh"
 #include "ntt_large.cuh"
 #include "ntt_small.cuh"
+#include "keyswitch.cuh"
 #include "plan.h"
 
 using namespace rnt;
@@ -489,6 +490,115 @@ static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, co
   return after_launch();
 }
 
+// BConv tables from basis {q_i} (L) to {p_j} (K) (reading G3):
+// src[i].qhatinv = (Q/q_i)^{-1} mod q_i, qp[j][i] = Q/q_i mod p_j, Shoup pairs.
+static void bconv_tables(const uint64_t* q, uint32_t L, const uint64_t* p, uint32_t K, std::vector<BcMod>& src,
+                         std::vector<BcMod>& dst, std::vector<TW>& qp) {
+  src.assign(L, BcMod{});
+  dst.assign(K, BcMod{});
+  qp.assign((size_t)K * L, TW{0, 0});
+  for (uint32_t i = 0; i < L; ++i) {
+    uint64_t h = 1 % q[i];
+    for (uint32_t k = 0; k < L; ++k)
+      if (k != i) h = hp_mulmod(h, q[k] % q[i], q[i]);
+    const uint64_t hinv = hp_powmod(h, q[i] - 2, q[i]);
+    src[i].m = q[i];
+    src[i].m2 = 2 * q[i];
+    src[i].qhatinv = TW{hinv, (uint64_t)(((unsigned __int128)hinv << 64) / q[i])};
+  }
+  for (uint32_t j = 0; j < K; ++j) {
+    dst[j].m = p[j];
+    dst[j].m2 = 2 * p[j];
+    dst[j].qhatinv = TW{0, 0};
+    for (uint32_t i = 0; i < L; ++i) {
+      uint64_t h = 1 % p[j];
+      for (uint32_t k = 0; k < L; ++k)
+        if (k != i) h = hp_mulmod(h, q[k] % p[j], p[j]);
+      qp[(size_t)j * L + i] = TW{h, (uint64_t)(((unsigned __int128)h << 64) / p[j])};
+    }
+  }
+}
+
+// Fused ModUp -> NTT -> key product for one-prime digits (keyswitch.cuh):
+// column pass with the lift on load (k_col_fwd<.., MODUP>), then the row pass
+// with the key multiply-accumulate (k_row_mac).  E: [dnum][LK][N] scratch.
+// Digit split of the fused key product (k_row_mac blockIdx.z): dnum digits in
+// `split` partial sums, added by k_ks_sum.  Env RNT_KS_SPLIT overrides.
+static uint32_t ks_split(uint32_t dnum) {
+  static int v = -1;
+  if (v < 0) {
+    const char* ev = getenv("RNT_KS_SPLIT");
+    v = ev ? atoi(ev) : 1;
+    if (v < 1) v = 1;
+    if (v > 8) v = 8;
+  }
+  return (uint32_t)v < dnum ? (uint32_t)v : dnum;
+}
+
+template <int LOGN>
+static rnt_status ks_fused_launch(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk, uint32_t dnum,
+                                  uint32_t split, const KsMod* km, cudaStream_t st) {
+  using P = TwoPass<LOGN>;
+  const uint32_t LK = qp->L;
+  const uint64_t units = (uint64_t)dnum * LK;
+  for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
+    const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
+    dim3 g(P::Cn / kColTile, (unsigned)cnt);
+    k_col_fwd<LOGN, kColTile, true><<<g, kColTile * P::T1, 0, st>>>(E, x, qp->d_col_fwd, qp->d_lc, LK, dnum, y0);
+    rnt_status s = after_launch();
+    if (s != RNT_OK) return s;
+  }
+  constexpr int RPC = P::RPC;
+  const size_t smem = (size_t)2 * RPC * P::Cn * 8;
+  static bool attr_set = false;  // benign race: idempotent attribute call
+  if (!attr_set) {
+    RNT_CUDA(cudaFuncSetAttribute(k_row_mac<LOGN, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  dim3 g(P::R / RPC, LK, split);
+  k_row_mac<LOGN, RPC><<<g, RPC * P::T2, smem, st>>>(u, E, evk, qp->d_fwd, qp->d_lc, LK, dnum, split);
+  rnt_status s = after_launch();
+  if (s != RNT_OK || split == 1) return s;
+  const uint64_t total = 2ull * LK << LOGN;
+  uint64_t blocks = (total + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  k_ks_sum<<<(unsigned)blocks, 256, 0, st>>>(u, split, km, LK, LOGN);
+  return after_launch();
+}
+
+static rnt_status ks_fused(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk, uint32_t dnum,
+                           uint32_t split, const KsMod* km, cudaStream_t st) {
+  switch (qp->logn) {
+    case 11: return ks_fused_launch<11>(qp, u, E, x, evk, dnum, split, km, st);
+    case 12: return ks_fused_launch<12>(qp, u, E, x, evk, dnum, split, km, st);
+    case 13: return ks_fused_launch<13>(qp, u, E, x, evk, dnum, split, km, st);
+    case 14: return ks_fused_launch<14>(qp, u, E, x, evk, dnum, split, km, st);
+    case 15: return ks_fused_launch<15>(qp, u, E, x, evk, dnum, split, km, st);
+    case 16: return ks_fused_launch<16>(qp, u, E, x, evk, dnum, split, km, st);
+    default: return RNT_E_UNSUPPORTED_N;
+  }
+}
+
+static inline uint64_t* U(u64* p) { return reinterpret_cast<uint64_t*>(p); }
+static inline const uint64_t* U(const u64* p) { return reinterpret_cast<const uint64_t*>(p); }
+
+struct rnt_keyswitch_s {
+  int device = 0;
+  uint32_t logn = 0, L = 0, K = 0, LK = 0, dnum = 0, alpha = 0;
+  rnt_plan_s* qp = nullptr;  // borrowed: extended-basis plan (Q then P)
+  rnt_plan_s* q = nullptr;   // borrowed: Q plan
+  KsMod* d_km = nullptr;     // [LK]
+  TW* d_tab = nullptr;       // [dnum][LK][alpha]
+  BcMod* d_bsrc = nullptr;   // ModDown BConv P -> Q
+  BcMod* d_bdst = nullptr;
+  TW* d_bqp = nullptr;
+  u64* d_ws = nullptr;       // x [L][N] | E [dnum][LK][N] | u [2][LK][N] | uP [2][K][N] | w [2][L][N]
+  uint32_t split = 1;        // digit split of the fused key product (u region holds `split` partial sums)
+  bool fused = false;        // N >= 2^11, one-prime digits: ModUp in the column pass, key product in the row pass
+  std::mutex mu;             // one apply at a time per handle (the workspace is shared)
+};
+
 extern "C" {
 
 const char* rnt_status_string(rnt_status s) {
@@ -767,30 +877,12 @@ rnt_status rnt_bconv_create(rnt_bconv* out, rnt_plan from, rnt_plan to) {
   rnt_status s = check_plan_device(from);
   if (s != RNT_OK) return s;
   const uint32_t L = from->L, K = to->L;
-  std::vector<BcMod> src(L), dst(K);
-  std::vector<TW> qp((size_t)K * L);
-  for (uint32_t i = 0; i < L; ++i) {
-    const uint64_t q = from->limbs[i].q;
-    uint64_t h = 1 % q;
-    for (uint32_t k = 0; k < L; ++k)
-      if (k != i) h = hp_mulmod(h, from->limbs[k].q % q, q);
-    const uint64_t hinv = hp_powmod(h, q - 2, q);
-    src[i].m = q;
-    src[i].m2 = 2 * q;
-    src[i].qhatinv = TW{hinv, (uint64_t)(((unsigned __int128)hinv << 64) / q)};
-  }
-  for (uint32_t j = 0; j < K; ++j) {
-    const uint64_t p = to->limbs[j].q;
-    dst[j].m = p;
-    dst[j].m2 = 2 * p;
-    dst[j].qhatinv = TW{0, 0};
-    for (uint32_t i = 0; i < L; ++i) {
-      uint64_t h = 1 % p;
-      for (uint32_t k = 0; k < L; ++k)
-        if (k != i) h = hp_mulmod(h, from->limbs[k].q % p, p);
-      qp[(size_t)j * L + i] = TW{h, (uint64_t)(((unsigned __int128)h << 64) / p)};
-    }
-  }
+  std::vector<uint64_t> fq(L), tq(K);
+  for (uint32_t i = 0; i < L; ++i) fq[i] = from->limbs[i].q;
+  for (uint32_t j = 0; j < K; ++j) tq[j] = to->limbs[j].q;
+  std::vector<BcMod> src, dst;
+  std::vector<TW> qp;
+  bconv_tables(fq.data(), L, tq.data(), K, src, dst, qp);
   rnt_bconv_s* c = new (std::nothrow) rnt_bconv_s;
   if (!c) return RNT_E_OOM;
   c->device = from->device;
@@ -839,6 +931,206 @@ rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint3
   k_bconv<<<grid, kBcTile, smem, (cudaStream_t)stream>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in),
                                                          c->d_src, c->d_dst, c->d_qhat_p, c->L, c->K, c->logn);
   return after_launch();
+}
+
+rnt_status rnt_keyswitch_destroy(rnt_keyswitch ks) {
+  if (!ks) return RNT_OK;
+  cudaFree(ks->d_km);
+  cudaFree(ks->d_tab);
+  cudaFree(ks->d_bsrc);
+  cudaFree(ks->d_bdst);
+  cudaFree(ks->d_bqp);
+  cudaFree(ks->d_ws);
+  delete ks;
+  return RNT_OK;
+}
+
+rnt_status rnt_keyswitch_create(rnt_keyswitch* out, rnt_plan q_plan, rnt_plan qp_plan, uint32_t dnum) {
+  if (!out || !q_plan || !qp_plan) return RNT_E_INVALID_ARG;
+  *out = nullptr;
+  if (q_plan->is_view || qp_plan->is_view) return RNT_E_INVALID_ARG;
+  const uint32_t L = q_plan->L, LK = qp_plan->L;
+  if (q_plan->logn != qp_plan->logn || q_plan->device != qp_plan->device || LK <= L || LK - L > 192)
+    return RNT_E_INVALID_ARG;
+  for (uint32_t i = 0; i < L; ++i)
+    if (q_plan->limbs[i].q != qp_plan->limbs[i].q || q_plan->limbs[i].psi != qp_plan->limbs[i].psi)
+      return RNT_E_INVALID_ARG;
+  if (dnum == 0 || dnum > L) return RNT_E_INVALID_ARG;
+  const uint32_t alpha = (L + dnum - 1) / dnum;
+  if ((dnum - 1) * alpha >= L || alpha > 192) return RNT_E_INVALID_ARG;  // every digit non-empty
+  rnt_status s = check_plan_device(q_plan);
+  if (s != RNT_OK) return s;
+  const uint32_t K = LK - L;
+  std::vector<uint64_t> m(LK);
+  unsigned __int128 mmax = 0;
+  for (uint32_t t = 0; t < LK; ++t) {
+    m[t] = qp_plan->limbs[t].q;
+    if (m[t] > mmax) mmax = m[t];
+  }
+  // k_ks_mac sums dnum exact products in 128 bits
+  if (mmax * mmax > (~(unsigned __int128)0) / dnum) return RNT_E_INVALID_ARG;
+  std::vector<KsMod> km(LK);
+  for (uint32_t t = 0; t < LK; ++t) {
+    const HostLimb& h = qp_plan->limbs[t];
+    km[t].m = h.q;
+    km[t].m2 = h.q2;
+    km[t].qinv = h.qinv;
+    km[t].r2 = h.r2;
+    km[t].one = TW{1, (uint64_t)(((unsigned __int128)1 << 64) / h.q)};
+    km[t].pinv = TW{0, 0};
+    km[t].qhatinv = TW{0, 0};
+  }
+  for (uint32_t i = 0; i < L; ++i) {
+    uint64_t pp = 1;
+    for (uint32_t t = L; t < LK; ++t) pp = hp_mulmod(pp, m[t] % m[i], m[i]);
+    const uint64_t pinv = hp_powmod(pp, m[i] - 2, m[i]);
+    km[i].pinv = TW{pinv, (uint64_t)(((unsigned __int128)pinv << 64) / m[i])};
+  }
+  // ModUp tables per digit (reading KS2: digit j = limbs [j alpha, min(L, (j+1) alpha)))
+  std::vector<TW> tab((size_t)dnum * LK * alpha, TW{0, 0});
+  for (uint32_t j = 0; j < dnum; ++j) {
+    const uint32_t lo = j * alpha, hi = (lo + alpha < L) ? lo + alpha : L;
+    std::vector<BcMod> src, dst;
+    std::vector<TW> qp;
+    bconv_tables(m.data() + lo, hi - lo, m.data(), LK, src, dst, qp);
+    for (uint32_t i = lo; i < hi; ++i) km[i].qhatinv = src[i - lo].qhatinv;
+    for (uint32_t t = 0; t < LK; ++t)
+      for (uint32_t i = 0; i < hi - lo; ++i) tab[((size_t)j * LK + t) * alpha + i] = qp[(size_t)t * (hi - lo) + i];
+  }
+  std::vector<BcMod> bsrc, bdst;
+  std::vector<TW> bqp;
+  bconv_tables(m.data() + L, K, m.data(), L, bsrc, bdst, bqp);
+
+  rnt_keyswitch_s* ks = new (std::nothrow) rnt_keyswitch_s;
+  if (!ks) return RNT_E_OOM;
+  ks->device = q_plan->device;
+  ks->logn = q_plan->logn;
+  ks->L = L;
+  ks->K = K;
+  ks->LK = LK;
+  ks->dnum = dnum;
+  ks->alpha = alpha;
+  ks->q = q_plan;
+  ks->qp = qp_plan;
+  {
+    uint64_t qmax = 0, mmin = ~0ull;
+    for (uint32_t i = 0; i < L; ++i) qmax = m[i] > qmax ? m[i] : qmax;
+    for (uint32_t t = 0; t < LK; ++t) mmin = m[t] < mmin ? m[t] : mmin;
+    static int force_unfused = -1;
+    if (force_unfused < 0) {
+      const char* ev = getenv("RNT_KS_UNFUSED");
+      force_unfused = ev && atoi(ev) > 0;
+    }
+    ks->fused = !force_unfused && ks->logn >= 11 && alpha == 1 && qmax / 2 < mmin;
+    ks->split = ks->fused ? ks_split(dnum) : 1;
+  }
+  const size_t n = (size_t)1 << ks->logn;
+  const size_t ws =
+      n * ((size_t)L + (size_t)dnum * LK + 2 * (size_t)LK * ks->split + 2 * (size_t)K + 2 * (size_t)L);
+  cudaError_t e;
+  if ((e = cudaMalloc(&ks->d_km, sizeof(KsMod) * LK)) != cudaSuccess ||
+      (e = cudaMalloc(&ks->d_tab, sizeof(TW) * tab.size())) != cudaSuccess ||
+      (e = cudaMalloc(&ks->d_bsrc, sizeof(BcMod) * K)) != cudaSuccess ||
+      (e = cudaMalloc(&ks->d_bdst, sizeof(BcMod) * L)) != cudaSuccess ||
+      (e = cudaMalloc(&ks->d_bqp, sizeof(TW) * bqp.size())) != cudaSuccess ||
+      (e = cudaMalloc(&ks->d_ws, sizeof(u64) * ws)) != cudaSuccess ||
+      (e = cudaMemcpy(ks->d_km, km.data(), sizeof(KsMod) * LK, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(ks->d_tab, tab.data(), sizeof(TW) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(ks->d_bsrc, bsrc.data(), sizeof(BcMod) * K, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(ks->d_bdst, bdst.data(), sizeof(BcMod) * L, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(ks->d_bqp, bqp.data(), sizeof(TW) * bqp.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    rnt_keyswitch_destroy(ks);
+    return cuda_fail(e);
+  }
+  *out = ks;
+  return RNT_OK;
+}
+
+rnt_status rnt_keyswitch_query(rnt_keyswitch ks, uint32_t* alpha, uint64_t* workspace_bytes) {
+  if (!ks) return RNT_E_INVALID_ARG;
+  const size_t n = (size_t)1 << ks->logn;
+  if (alpha) *alpha = ks->alpha;
+  if (workspace_bytes)
+    *workspace_bytes = 8 * n * ((size_t)ks->L + (size_t)ks->dnum * ks->LK + 2 * (size_t)ks->LK * ks->split +
+                                2 * (size_t)ks->K + 2 * (size_t)ks->L);
+  return RNT_OK;
+}
+
+rnt_status rnt_keyswitch_apply(rnt_keyswitch ks, uint64_t* out_, const uint64_t* d_, const uint64_t* evk_,
+                               const uint64_t* add0_, void* stream) {
+  if (!ks) return RNT_E_INVALID_ARG;
+  if (!out_ || !d_ || !evk_ || !aligned16(out_) || !aligned16(d_) || !aligned16(evk_) ||
+      (add0_ && !aligned16(add0_)))
+    return RNT_E_INVALID_ARG;
+  rnt_status s = check_plan_device(ks->q);
+  if (s != RNT_OK) return s;
+  if ((s = debug_validate(ks->q, d_, ks->L, (cudaStream_t)stream)) != RNT_OK) return s;
+  std::lock_guard<std::mutex> g(ks->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  u64* out = reinterpret_cast<u64*>(out_);
+  const u64* d = reinterpret_cast<const u64*>(d_);
+  const u64* evk = reinterpret_cast<const u64*>(evk_);
+  const u64* add0 = reinterpret_cast<const u64*>(add0_);
+  const uint32_t L = ks->L, K = ks->K, LK = ks->LK, logn = ks->logn;
+  const size_t n = (size_t)1 << logn;
+  u64* x = ks->d_ws;
+  u64* E = x + (size_t)L * n;
+  u64* u = E + (size_t)ks->dnum * LK * n;
+  u64* up = u + 2 * (size_t)LK * n * ks->split;
+  u64* w = up + 2 * (size_t)K * n;
+  // 1. x = INTT_Q(d)
+  if ((s = run_op(ks->q, 1, U(x), U(d), nullptr, 0, 1, st)) != RNT_OK) return s;
+  // 2-3 fused: lift on load + column pass, row pass + key product
+  if (ks->fused) {
+    if ((s = ks_fused(ks->qp, u, E, x, evk, ks->dnum, ks->split, ks->d_km, st)) != RNT_OK) return s;
+  } else {
+  // 2. ModUp every digit, then NTT of the extended polynomials (batch = dnum)
+  {
+    const size_t smem = (size_t)ks->alpha * kKsTile * 8;
+    static size_t attr = 0;  // benign race: idempotent attribute call
+    if (smem > 48 * 1024 && attr < smem) {
+      RNT_CUDA(cudaFuncSetAttribute(k_modup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    dim3 grid((unsigned)((n + kKsTile - 1) / kKsTile), ks->dnum);
+    k_modup<<<grid, kKsTile, smem, st>>>(E, x, ks->d_km, ks->d_tab, L, LK, ks->alpha, logn);
+    if ((s = after_launch()) != RNT_OK) return s;
+  }
+  if ((s = run_op(ks->qp, 0, U(E), U(E), nullptr, 0, ks->dnum, st)) != RNT_OK) return s;
+  // 3. key inner product
+  {
+    const uint64_t per = (uint64_t)LK * n;
+    uint64_t blocks = (per + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    k_ks_mac<<<(unsigned)blocks, 256, 0, st>>>(u, E, evk, ks->d_km, ks->dnum, LK, logn);
+    if ((s = after_launch()) != RNT_OK) return s;
+  }
+  }
+  // 4. ModDown: INTT of the P limbs, BConv P -> Q, NTT_Q, (u - w) P^{-1}
+  {
+    rnt_plan_s pv;
+    make_view(ks->qp, L, K, &pv);
+    for (int k = 0; k < 2; ++k)
+      if ((s = run_op(&pv, 1, U(up + (size_t)k * K * n), U(u + ((size_t)k * LK + L) * n), nullptr, 0, 1, st)) != RNT_OK)
+        return s;
+    const size_t smem = (size_t)K * kBcTile * 8;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+      RNT_CUDA(cudaFuncSetAttribute(k_bconv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    dim3 grid((unsigned)((n + kBcTile - 1) / kBcTile), 2);
+    k_bconv<<<grid, kBcTile, smem, st>>>(w, up, ks->d_bsrc, ks->d_bdst, ks->d_bqp, K, L, logn);
+    if ((s = after_launch()) != RNT_OK) return s;
+    if ((s = run_op(ks->q, 0, U(w), U(w), nullptr, 0, 2, st)) != RNT_OK) return s;
+    const uint64_t total = 2 * (uint64_t)L * n;
+    uint64_t blocks = (total + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    k_moddown<<<(unsigned)blocks, 256, 0, st>>>(out, u, w, add0, ks->d_km, L, LK, logn);
+    return after_launch();
+  }
 }
 
 rnt_status rnt_external_product(rnt_plan p, uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat,

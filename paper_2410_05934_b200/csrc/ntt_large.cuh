@@ -53,7 +53,10 @@ __device__ __forceinline__ int row_swz(int c) {
 // ============================== pass 1 (columns) ==============================
 // Forward: CT stages 0..n1-1 on columns [cb*16, cb*16+16) of unit u.
 // MODE 0: plain forward (in -> out).
-template <int LOGN, int CT = kColTile>
+// MODUP (key switching, keyswitch.cuh): unit (poly j, limb t) reads limb j of a
+// single L-limb polynomial (one-prime digits, reading KS2 with alpha = 1) and
+// lifts it to q_t on load: x mod q_t = x - q_t if x >= q_t (requires q_j < 2 q_t).
+template <int LOGN, int CT = kColTile, bool MODUP = false>
 __global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
 k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
@@ -68,8 +71,14 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
   const TW* T = tw_col + (size_t)l * P::R;
   const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
   u64 x[kEl];
+  if constexpr (MODUP) {
+    const size_t ibase = (y % B) * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(r0 + P::T1 * i) * P::Cn];
+    for (int i = 0; i < kEl; ++i) x[i] = csub(__ldg(in + ibase + (size_t)(r0 + P::T1 * i) * P::Cn), q);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(r0 + P::T1 * i) * P::Cn];
+  }
   // sub-pass A: stages 0..3, twiddle w[2^s + (i >> (4-s))] (uniform)
   sfor<0, 4>([&](auto S_) {
     constexpr int s = decltype(S_)::value;
@@ -310,6 +319,67 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   }
 #pragma unroll
   for (int i = 0; i < kEl; ++i) out[rowoff + c0 + P::T2 * i] = x[i];
+}
+
+// ============================ pass 2 + key product ============================
+
+// Key switching (keyswitch.cuh, rnt_keyswitch_apply): for the RPC rows r of
+// limb t, run the forward row stages of every digit's extended polynomial
+// (E: [dnum][LK][N], column pass done) and accumulate the products with the
+// key rows in shared memory, u_k[t] = sum_j NTT(e_j)[t] (.) evk[j][k][t]:
+// the NTT-form extended polynomials never go back to HBM.  Montgomery
+// products, accumulators kept in [0, 2q); u written canonical.
+template <int LOGN, int RPC_>
+__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2)
+k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict__ evk,
+          const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t LK, uint32_t dnum,
+          uint32_t dsplit) {
+  // blockIdx.z = s: digits [s dnum / dsplit, (s+1) dnum / dsplit) into partial sum s
+  // (uo + s 2 LK N); dsplit > 1 evens out the last wave, k_ks_sum adds the parts.
+  using P = TwoPass<LOGN>;
+  constexpr size_t N = (size_t)P::R * P::Cn;
+  __shared__ __align__(16) u64 sbuf[RPC_ * P::ROWBUF];
+  extern __shared__ __align__(16) u64 acc[];   // [2][RPC_][Cn]
+  const int c0 = threadIdx.x % P::T2;
+  const int rr = threadIdx.x / P::T2;
+  const int r = blockIdx.x * RPC_ + rr;
+  const uint32_t t = blockIdx.y;
+  const u64 q = lc[t].q, q2 = lc[t].q2, qinv = lc[t].qinv;
+  u64* rb = sbuf + rr * P::ROWBUF;
+  u64* a0 = acc + (size_t)rr * P::Cn + c0;
+  u64* a1 = acc + (size_t)(RPC_ + rr) * P::Cn + c0;
+  const TW* Tf = tw_row_fwd + ((size_t)t * P::R + r) * P::Cn;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) a0[P::T2 * i] = a1[P::T2 * i] = 0;
+  const size_t roff = (size_t)r * P::Cn + c0;
+  const uint32_t jb = blockIdx.z * dnum / dsplit, je = (blockIdx.z + 1) * dnum / dsplit;
+  uo += (size_t)blockIdx.z * 2 * LK * N;
+  for (uint32_t j = jb; j < je; ++j) {
+    const u64* src = E + ((size_t)j * LK + t) * N + roff;
+    u64 x[kEl];
+#pragma unroll
+    for (int i = 0; i < kEl; ++i) x[i] = __ldcs(src + P::T2 * i);
+    row_fwd_A<LOGN>(x, Tf, q, q2);
+    row_A_to_B<LOGN>(x, rb, c0);
+    row_fwd_B<LOGN>(x, Tf, c0, q, q2);
+    row_B_to_A<LOGN>(x, rb, c0);
+    const u64* k0 = evk + ((size_t)(2 * j) * LK + t) * N + roff;
+    const u64* k1 = k0 + (size_t)LK * N;
+#pragma unroll
+    for (int i = 0; i < kEl; ++i) {
+      const u64 b0 = __ldcs(k0 + P::T2 * i), b1 = __ldcs(k1 + P::T2 * i);
+      a0[P::T2 * i] = csub(a0[P::T2 * i] + mont_mul(x[i], b0, q, qinv), q2);
+      a1[P::T2 * i] = csub(a1[P::T2 * i] + mont_mul(x[i], b1, q, qinv), q2);
+    }
+  }
+  const u64 r2 = lc[t].r2;
+  u64* o0 = uo + (size_t)t * N + roff;
+  u64* o1 = uo + ((size_t)LK + t) * N + roff;
+#pragma unroll
+  for (int i = 0; i < kEl; ++i) {
+    o0[P::T2 * i] = canon2(mont_mul(a0[P::T2 * i], r2, q, qinv), q);
+    o1[P::T2 * i] = canon2(mont_mul(a1[P::T2 * i], r2, q, qinv), q);
+  }
 }
 
 // ============================ pass 2, warp engine =============================

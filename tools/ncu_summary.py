@@ -51,7 +51,7 @@ def scale(val, unit, want):
     if want == "MB" and unit in f:
         return val * f[unit]
     if want == "us":
-        return {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0) * val
+        return {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0) * val
     if want == "MHz":
         return {"hz": 1e-6, "Khz": 1e-3, "Mhz": 1.0, "Ghz": 1e3, "cycle/second": 1e-6,
                 "cycle/nsecond": 1e3, "cycle/usecond": 1.0}.get(unit, 1.0) * val
