@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "librnsntt.so")
 SOURCES = ["api.cu", "plan.cpp"]
-HEADERS = ["modarith.cuh", "ntt_small.cuh", "ntt_large.cuh", "plan.h"]
+HEADERS = ["modarith.cuh", "ntt_small.cuh", "ntt_large.cuh", "keyswitch.cuh", "plan.h"]
 
 NVCC_FLAGS = [
     "-O3",
@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
+    extra = os.environ.get("RNT_NVCC_EXTRA", "").split()   # experiments only (e.g. -DRNT_ROW_MINB=3)
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)

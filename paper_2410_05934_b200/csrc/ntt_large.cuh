@@ -257,8 +257,15 @@ __device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
 // MODE 0: forward rows (CT stages n1..n-1, canonical output)
 // MODE 1: inverse rows (GS stages n-1..n1, lazy [0,2q) output for k_col_inv)
 // MODE 2: fused forward rows -> (.) b_hat (Montgomery) -> inverse rows
+// (RNT_ROW_MINB: experiment knob; an explicit min-blocks of 1 measured 18 % slower
+// than leaving it unspecified, 3 about equal.)
+#ifdef RNT_ROW_MINB
+#define RNT_ROW_BOUNDS(t) __launch_bounds__(t, RNT_ROW_MINB)
+#else
+#define RNT_ROW_BOUNDS(t) __launch_bounds__(t)
+#endif
 template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC>
-__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2)
+__global__ void RNT_ROW_BOUNDS(RPC_ * TwoPass<LOGN>::T2)
 k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
       const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
