@@ -1190,7 +1190,7 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   const size_t n = (size_t)1 << p->logn;
   const size_t unit_bytes = n * 8;
   const size_t total_units = (size_t)batch * p->L;
-  // Chunking: ~8 MiB chunks over polynomials (batch > 1) or limbs (batch == 1),
+  // Chunking: chunks over polynomials (batch > 1) or limbs (batch == 1),
   // round-robin over three internal streams so H2D copy, kernels and D2H copy
   // of successive chunks overlap.  Fork/join with the caller's stream by events.
   static size_t target = 0;  // chunk bytes (tuning knob RNT_CHUNK_MB, default 16 MiB, measured best)
@@ -1198,16 +1198,35 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
     const char* ev = getenv("RNT_CHUNK_MB");
     target = (size_t)(ev && atoi(ev) > 0 ? atoi(ev) : 16) << 20;
   }
-  size_t per_chunk_units = target / unit_bytes;
-  if (per_chunk_units < 1) per_chunk_units = 1;
-  uint32_t nchunks;
-  if (batch > 1) {
-    size_t polys = per_chunk_units / p->L;
-    if (polys < 1) polys = 1;
-    nchunks = (uint32_t)((batch + polys - 1) / polys);
-  } else {
-    nchunks = (uint32_t)((p->L + per_chunk_units - 1) / per_chunk_units);
+  // Granule = one polynomial (batch > 1) or one limb (batch == 1).  Chunks of
+  // `target` bytes, except that the first and last chunks ramp (target/8,
+  // /4, /2, ...) so the copy engines start and drain sooner (env RNT_CHUNK_RAMP=0: uniform).
+  static int ramp = -1;
+  if (ramp < 0) {
+    const char* ev = getenv("RNT_CHUNK_RAMP");
+    ramp = ev ? atoi(ev) > 0 : 1;
   }
+  const size_t gbytes = batch > 1 ? (size_t)p->L * unit_bytes : unit_bytes;
+  const size_t G = batch > 1 ? batch : p->L;
+  size_t T = target / gbytes;
+  if (T < 1) T = 1;
+  std::vector<size_t> front, back;
+  {
+    size_t left = G;
+    const size_t r0 = ramp ? (T / 8 ? T / 8 : 1) : T;
+    for (size_t sz = r0; left; sz = sz * 2 < T ? sz * 2 : T) {
+      const size_t a = sz < left ? sz : left;
+      front.push_back(a);
+      left -= a;
+      if (!left) break;
+      const size_t b = sz < left ? sz : left;
+      back.push_back(b);
+      left -= b;
+    }
+  }
+  std::vector<size_t> csz(front);
+  csz.insert(csz.end(), back.rbegin(), back.rend());
+  const uint32_t nchunks = (uint32_t)csz.size();
   if (nchunks <= 1) {
     RNT_CUDA(cudaMemcpyAsync(dev_ws, in_host, total_units * unit_bytes, cudaMemcpyHostToDevice, st));
     s = run_op(p, (int)op, dev_ws, dev_ws, b_dev, b_broadcast ? 1 : 0, batch, st);
@@ -1230,25 +1249,20 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   cudaEvent_t fork = p->ev_pool[0];
   RNT_CUDA(cudaEventRecord(fork, st));
   for (int i = 0; i < 3; ++i) RNT_CUDA(cudaStreamWaitEvent(p->aux[i], fork, 0));
-  for (uint32_t c = 0; c < nchunks && s == RNT_OK; ++c) {
+  size_t g0 = 0;
+  for (uint32_t c = 0; c < nchunks && s == RNT_OK; g0 += csz[c], ++c) {
     size_t u0, nu;
     const uint64_t* bchunk = b_dev;
     rnt_plan_s view;
     const rnt_plan_s* pp = p;
     uint32_t cb = batch;
     if (batch > 1) {
-      const uint32_t per = (batch + nchunks - 1) / nchunks;
-      const uint32_t b0 = c * per;
-      if (b0 >= batch) break;
-      cb = batch - b0 < per ? batch - b0 : per;
-      u0 = (size_t)b0 * p->L;
+      cb = (uint32_t)csz[c];
+      u0 = g0 * p->L;
       nu = (size_t)cb * p->L;
       if (bop && !b_broadcast) bchunk = b_dev + u0 * n;
     } else {
-      const uint32_t per = (p->L + nchunks - 1) / nchunks;
-      const uint32_t l0 = c * per;
-      if (l0 >= p->L) break;
-      const uint32_t nl = p->L - l0 < per ? p->L - l0 : per;
+      const uint32_t l0 = (uint32_t)g0, nl = (uint32_t)csz[c];
       make_view(p, l0, nl, &view);
       pp = &view;
       u0 = l0;
