@@ -19,6 +19,7 @@
 #include "ntt_large.cuh"
 #include "ntt_small.cuh"
 #include "keyswitch.cuh"
+#include "ntt_cluster.cuh"
 #include "plan.h"
 
 using namespace rnt;
@@ -403,8 +404,93 @@ static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in,
   }
 }
 
+// Single-launch cluster path (ntt_cluster.cuh) for latency-bound jobs: a
+// cluster of C CTAs owns one limb on chip.  Used when batch * L is at most
+// cluster_units() (env RNT_CLUSTER_UNITS; 0 disables).
+static int cluster_units() {
+  static int v = -1;
+  if (v < 0) {
+    const char* ev = getenv("RNT_CLUSTER_UNITS");
+    v = ev ? atoi(ev) : 2;
+  }
+  return v;
+}
+
+template <int LOGN, int C, int MODE>
+static rnt_status launch_cluster_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                   uint32_t batch, cudaStream_t st) {
+  using G = ClusterGeo<LOGN, C>;
+  auto kern = k_cluster<LOGN, C, MODE>;
+  static bool attr_set = false;  // benign race: idempotent attribute calls
+  if (!attr_set) {
+    RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    if (C > 8) RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_set = true;
+  }
+  const uint64_t units = (uint64_t)batch * p->L;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * C), 1, 1);
+  cfg.blockDim = dim3(G::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  const TW* cf = p->d_col_fwd;
+  const TW* ci = p->d_col_inv;
+  const TW* rf = p->d_fwd;
+  const LimbC* lcp = p->d_lc;
+  RNT_CUDA(cudaLaunchKernelEx(&cfg, kern, out, in, bop, bcast, cf, ci, rf, lcp, p->L));
+  return after_launch();
+}
+
+template <int LOGN, int C>
+static rnt_status cluster_op_c(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                               uint32_t batch, cudaStream_t st) {
+  switch (op) {
+    case 0: return launch_cluster_v<LOGN, C, 0>(p, out, in, bop, bcast, batch, st);
+    case 1: return launch_cluster_v<LOGN, C, 1>(p, out, in, bop, bcast, batch, st);
+    case 2: return launch_cluster_v<LOGN, C, 2>(p, out, in, bop, bcast, batch, st);
+    default: return RNT_E_INVALID_ARG;
+  }
+}
+
+template <int LOGN>
+static rnt_status cluster_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                             uint32_t batch, cudaStream_t st) {
+  // cluster size: 8 CTAs up to 2^14, 16 above (measured, single-polynomial
+  // latency); env RNT_CLUSTER_C = 8 or 16 forces one
+  static int csz = -1;
+  if (csz < 0) {
+    const char* ev = getenv("RNT_CLUSTER_C");
+    csz = ev ? (atoi(ev) == 8 ? 8 : 16) : 0;
+  }
+  if (csz == 8 || (csz == 0 && LOGN <= 14)) return cluster_op_c<LOGN, 8>(p, op, out, in, bop, bcast, batch, st);
+  return cluster_op_c<LOGN, 16>(p, op, out, in, bop, bcast, batch, st);
+}
+
+static rnt_status cluster_dispatch(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                                   uint32_t batch, cudaStream_t st) {
+  switch (p->logn) {
+    case 11: return cluster_op<11>(p, op, out, in, bop, bcast, batch, st);
+    case 12: return cluster_op<12>(p, op, out, in, bop, bcast, batch, st);
+    case 13: return cluster_op<13>(p, op, out, in, bop, bcast, batch, st);
+    case 14: return cluster_op<14>(p, op, out, in, bop, bcast, batch, st);
+    case 15: return cluster_op<15>(p, op, out, in, bop, bcast, batch, st);
+    case 16: return cluster_op<16>(p, op, out, in, bop, bcast, batch, st);
+    default: return RNT_E_UNSUPPORTED_N;
+  }
+}
+
 static rnt_status large_dispatch(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop,
                                  int bcast, uint32_t batch, cudaStream_t st) {
+  const uint64_t units = (uint64_t)batch * p->L;
+  if (units == 0) return RNT_OK;
+  if (units <= (uint64_t)cluster_units()) return cluster_dispatch(p, op, out, in, bop, bcast, batch, st);
   switch (p->logn) {
     case 11: return large_op<11>(p, op, out, in, bop, bcast, batch, st);
     case 12: return large_op<12>(p, op, out, in, bop, bcast, batch, st);
@@ -797,6 +883,7 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
     rnt_status s = RNT_OK;
     for (int gi = 0; gi < split_g; ++gi) {
       const uint32_t l0 = gi * per;
+      if (l0 >= p->L) break;   // fewer windows than streams (e.g. L = 9, G = 4)
       const uint32_t nl = p->L - l0 < per ? p->L - l0 : per;
       rnt_plan_s view;
       make_view(p, l0, nl, &view);

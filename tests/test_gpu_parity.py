@@ -339,6 +339,33 @@ def test_limb_split_single_poly(logn, limbs, op):
     assert np.array_equal(from_dev(d), want)
 
 
+@pytest.mark.parametrize("logn", [11, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 1), (1, 2)])
+@pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_bcast"])
+def test_cluster_path(logn, limbs, batch, op):
+    """batch * L <= 2 at N >= 2^11 runs the single-launch cluster kernel
+    (ntt_cluster.cuh: column pass, DSMEM exchange, row pass, exchange, inverse columns)."""
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    n = 1 << logn
+    a = inputs.residues(41 + logn, batch, ps, n)
+    b = inputs.residues(42 + logn, 1 if op == "polymul_bcast" else batch, ps, n)
+    d = empty_dev(a.shape)
+    n0 = R.launch_count()
+    if op == "fwd":
+        R.ntt_forward(p, d, to_dev(a))
+        want = O.batch(O.OP_FWD, a, ps, psi)
+    elif op == "inv":
+        R.ntt_inverse(p, d, to_dev(a))
+        want = O.batch(O.OP_INV, a, ps, psi)
+    else:
+        bh = O.batch(O.OP_FWD, b, ps, psi)
+        R.polymul(p, d, to_dev(a), to_dev(bh), b_is_eval=True, b_broadcast=(op == "polymul_bcast"))
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, b_broadcast=(op == "polymul_bcast"))
+    assert R.launch_count() - n0 == 1          # one launch: the cluster kernel
+    assert np.array_equal(from_dev(d), want)
+
+
 VARIANT_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
@@ -363,7 +390,9 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
 
 @pytest.mark.parametrize("env", [{"RNT_SMALL_VARIANT": str(v)} for v in (1, 4, 5, 6, 7, 8, 11, 13)] +
                          [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)] +
-                         [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)])
+                         [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)] +
+                         [{"RNT_CLUSTER_C": "8"}, {"RNT_CLUSTER_C": "16"}, {"RNT_CLUSTER_UNITS": "0"},
+                          {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
