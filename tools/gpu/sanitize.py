@@ -22,7 +22,9 @@ def host(t):
 
 
 ok = True
-for logn, limbs, batch in ((4, 2, 5), (7, 1, 3), (10, 2, 3), (11, 2, 1), (16, 2, 2)):
+# (11,2,1), (16,1,1), (12,1,2): cluster kernel; (13,5,1): limb split over streams; (16,2,2): three kernels
+for logn, limbs, batch in ((4, 2, 5), (7, 1, 3), (10, 2, 3), (11, 2, 1), (16, 1, 1), (12, 1, 2), (13, 5, 1),
+                          (16, 2, 2)):
     ps = O.primes(logn, limbs)
     psi = [O.min_psi(q, logn) for q in ps]
     p = R.Plan(logn, ps)
@@ -41,4 +43,29 @@ for logn, limbs, batch in ((4, 2, 5), (7, 1, 3), (10, 2, 3), (11, 2, 1), (16, 2,
     ok &= np.array_equal(host(d), want)
     R.pointwise_mul(p, d, dev(a), dev(b))
     torch.cuda.synchronize()
+# key switching: fused (one-prime digits) and unfused (two-prime digits) paths
+for logn, L, K, dnum in ((11, 3, 1, 3), (11, 4, 2, 2)):
+    n = 1 << logn
+    mods = O.primes(logn, L + K)
+    qs, pp = mods[:L], mods[L:]
+    dd = inputs.residues(3, 1, qs, n)[0]
+    evk = inputs.residues(4, 2 * dnum, mods, n).reshape(dnum, 2, L + K, n)
+    a0 = inputs.residues(5, 1, qs, n)[0]
+    ks = R.KeySwitch(R.Plan(logn, qs), R.Plan(logn, mods), dnum)
+    out = torch.empty((2, L, n), dtype=torch.int64, device="cuda")
+    ks(out, dev(dd), dev(evk), add0=dev(a0))
+    ok &= np.array_equal(host(out), O.keyswitch(dd, evk, qs, pp, dnum, add0=a0))
+# automorphism and BConv
+ps = O.primes(11, 3)
+p = R.Plan(11, ps)
+a = inputs.residues(6, 2, ps, 1 << 11)
+d = torch.empty(a.shape, dtype=torch.int64, device="cuda")
+R.automorph(p, d, dev(a), 5, ntt_domain=False)
+ok &= np.array_equal(host(d)[1, 2], O.automorph(a[1, 2], ps[2], 5))
+pd = R.Plan(11, O.primes(11, 5)[3:])
+bc = R.BConv(p, pd)
+o2 = torch.empty((2, 2, 1 << 11), dtype=torch.int64, device="cuda")
+bc(o2, dev(a))
+ok &= np.array_equal(host(o2)[0], O.bconv(a[0], ps, O.primes(11, 5)[3:]))
+torch.cuda.synchronize()
 print("sanitize run ok" if ok else "MISMATCH")
