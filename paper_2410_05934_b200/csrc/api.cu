@@ -304,13 +304,22 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // CTA order for the two-pass kernels: block b -> (sub-block, poly, limb) with
 // the sub-block fastest, then the polynomial, then the limb, so CTAs that
 // share a limb's twiddle rows run back to back (L2 reuse across the batch).
-static int large_variant() {
-  static int v = -1;
-  if (v < 0) {
+// Large-N launch variant bits (env RNT_LARGE_VARIANT): 1 = 8-column pass-1
+// tiles, 2 = RPC/4 row CTAs, 4 = warp-engine rows (k_rows).  Unset: 5 for
+// N = 2^16 jobs of >= 192 limb-units (cfg4 0.827 -> 0.804 ms), else 0 (k_rows
+// under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
+static int large_variant_env() {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("RNT_LARGE_VARIANT");
-    v = e ? atoi(e) : 0;
+    v = e ? atoi(e) : -1;
   }
   return v;
+}
+static thread_local int g_large_auto = 0;   // set by large_op for the current call
+static int large_variant() {
+  const int v = large_variant_env();
+  return v >= 0 ? v : g_large_auto;
 }
 
 template <int LOGN, int CT>
@@ -389,6 +398,7 @@ template <int LOGN>
 static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
+  g_large_auto = (LOGN == 16 && (uint64_t)batch * p->L >= 192) ? 5 : 0;
   switch (op) {
     case 0:  // forward
       if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
