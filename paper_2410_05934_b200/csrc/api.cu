@@ -185,28 +185,51 @@ __global__ void k_check_range(const u64* __restrict__ x, const LimbC* __restrict
   if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
-static int g_num_sms = 0;
 static int num_sms() {
-  if (!g_num_sms) {
-    int d = 0;
+  static const int n = [] {
+    int d = 0, v = 0;
     cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, d);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+// Integer tuning knob from the environment, read once (thread-safe static init).
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// One-time (per kernel, per device) function attributes: dynamic shared memory
+// above 48 KB and, for 16-CTA clusters, the non-portable cluster size.
+template <typename K>
+static rnt_status ensure_attr(K kern, size_t smem, std::atomic<uint64_t>& done, bool nonportable = false) {
+  int d = 0;
+  RNT_CUDA(cudaGetDevice(&d));
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return RNT_OK;
+  RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (nonportable) RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  done.fetch_or(bit, std::memory_order_release);
+  return RNT_OK;
+}
+
+// Kernels whose shared memory depends on runtime sizes: set it on every call
+// above the default 48 KB (host-side, microseconds; not on the NTT hot path).
+template <typename K>
+static rnt_status set_smem(K kern, size_t smem) {
+  if (smem > 48 * 1024) RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return RNT_OK;
 }
 
 // ---------------------------------------------------------------- launchers
 template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
-  static bool attr_set = false;  // benign race: idempotent attribute call
+  static std::atomic<uint64_t> attr{0};
   const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
-  if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_warp<LOGN, MODE, W, MINB, SYNC, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr_set = true;
-  }
+  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM>, smem, attr); s != RNT_OK) return s;
   const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
@@ -224,25 +247,19 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
 // Tuning knob (benchmarks only): RNT_SMALL_VARIANT selects the N=2^10 launch
 // configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
 static int small_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RNT_SMALL_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
+  static const int v = env_int("RNT_SMALL_VARIANT", 0);
   return v;
 }
 
 template <int LOGN, int MODE, int W>
 static rnt_status launch_warp_tma(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                   uint32_t batch, cudaStream_t st) {
-  static int max_ctas_per_sm = 0;  // benign race: idempotent
+  static std::atomic<uint64_t> attr{0};
   const size_t smem = warp_tma_smem_bytes<W>();
-  if (!max_ctas_per_sm) {
-    RNT_CUDA(cudaFuncSetAttribute(k_warp_tma<LOGN, MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int n = 0;
-    RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_warp_tma<LOGN, MODE, W>, W * 32, smem));
-    max_ctas_per_sm = n > 0 ? n : 1;
-  }
+  if (rnt_status s = ensure_attr(k_warp_tma<LOGN, MODE, W>, smem, attr); s != RNT_OK) return s;
+  int max_ctas_per_sm = 0;
+  RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, k_warp_tma<LOGN, MODE, W>, W * 32, smem));
+  if (max_ctas_per_sm < 1) max_ctas_per_sm = 1;
   // persistent grid: as many warps as fit, then shrink so every warp runs the
   // same number of iterations (no tail imbalance).
   const uint64_t groups = ((uint64_t)batch + WarpCfg<LOGN>::P - 1) / WarpCfg<LOGN>::P;
@@ -309,11 +326,7 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // N = 2^16 jobs of >= 192 limb-units (cfg4 0.827 -> 0.804 ms), else 0 (k_rows
 // under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
 static int large_variant_env() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("RNT_LARGE_VARIANT");
-    v = e ? atoi(e) : -1;
-  }
+  static const int v = env_int("RNT_LARGE_VARIANT", -1);
   return v;
 }
 static thread_local int g_large_auto = 0;   // set by large_op for the current call
@@ -366,12 +379,9 @@ template <int LOGN, int MODE>
 static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                    uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
-  static bool attr_set = false;  // benign race: idempotent attribute call
+  static std::atomic<uint64_t> attr{0};
   const size_t smem = (size_t)kRowWarps * kWarpBuf * 8;
-  if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_rows<LOGN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  if (rnt_status s = ensure_attr(k_rows<LOGN, MODE>, smem, attr); s != RNT_OK) return s;
   constexpr int rows_per_cta = kRowWarps * (kWarpElems / P::Cn);
   const unsigned gx = (unsigned)((P::R + rows_per_cta - 1) / rows_per_cta);
   const uint64_t units = (uint64_t)batch * p->L;
@@ -418,11 +428,7 @@ static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in,
 // cluster of C CTAs owns one limb on chip.  Used when batch * L is at most
 // cluster_units() (env RNT_CLUSTER_UNITS; 0 disables).
 static int cluster_units() {
-  static int v = -1;
-  if (v < 0) {
-    const char* ev = getenv("RNT_CLUSTER_UNITS");
-    v = ev ? atoi(ev) : 2;
-  }
+  static const int v = env_int("RNT_CLUSTER_UNITS", 2);
   return v;
 }
 
@@ -431,12 +437,8 @@ static rnt_status launch_cluster_v(const rnt_plan_s* p, u64* out, const u64* in,
                                    uint32_t batch, cudaStream_t st) {
   using G = ClusterGeo<LOGN, C>;
   auto kern = k_cluster<LOGN, C, MODE>;
-  static bool attr_set = false;  // benign race: idempotent attribute calls
-  if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    if (C > 8) RNT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (rnt_status s = ensure_attr(kern, G::SMEM, attr, C > 8); s != RNT_OK) return s;
   const uint64_t units = (uint64_t)batch * p->L;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * C), 1, 1);
@@ -474,11 +476,10 @@ static rnt_status cluster_op(const rnt_plan_s* p, int op, u64* out, const u64* i
                              uint32_t batch, cudaStream_t st) {
   // cluster size: 8 CTAs up to 2^14, 16 above (measured, single-polynomial
   // latency); env RNT_CLUSTER_C = 8 or 16 forces one
-  static int csz = -1;
-  if (csz < 0) {
-    const char* ev = getenv("RNT_CLUSTER_C");
-    csz = ev ? (atoi(ev) == 8 ? 8 : 16) : 0;
-  }
+  static const int csz = [] {
+    const int v = env_int("RNT_CLUSTER_C", 0);
+    return v == 0 ? 0 : (v == 8 ? 8 : 16);
+  }();
   if (csz == 8 || (csz == 0 && LOGN <= 14)) return cluster_op_c<LOGN, 8>(p, op, out, in, bop, bcast, batch, st);
   return cluster_op_c<LOGN, 16>(p, op, out, in, bop, bcast, batch, st);
 }
@@ -525,11 +526,7 @@ static rnt_status check_plan_device(const rnt_plan_s* p) {
 static int num_sms();
 
 static bool debug_checks() {
-  static int on = -1;
-  if (on < 0) {
-    const char* ev = getenv("RNT_DEBUG");
-    on = ev && atoi(ev) > 0;
-  }
+  static const bool on = env_int("RNT_DEBUG", 0) > 0;
   return on;
 }
 
@@ -574,12 +571,9 @@ struct rnt_bconv_s {
 template <int LOGN>
 static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                  DigitSpec ds, cudaStream_t st) {
-  static bool attr_set = false;  // benign race: idempotent attribute call
+  static std::atomic<uint64_t> attr{0};
   const size_t smem = (size_t)2 * kWarpBuf * 8;
-  if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_extprod<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  if (rnt_status s = ensure_attr(k_extprod<LOGN>, smem, attr); s != RNT_OK) return s;
   const uint64_t per_cta = 2ull * (kWarpElems >> LOGN);
   const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
   k_extprod<LOGN><<<(unsigned)grid, 64, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc, n_slot, ds);
@@ -621,13 +615,10 @@ static void bconv_tables(const uint64_t* q, uint32_t L, const uint64_t* p, uint3
 // Digit split of the fused key product (k_row_mac blockIdx.z): dnum digits in
 // `split` partial sums, added by k_ks_sum.  Env RNT_KS_SPLIT overrides.
 static uint32_t ks_split(uint32_t dnum) {
-  static int v = -1;
-  if (v < 0) {
-    const char* ev = getenv("RNT_KS_SPLIT");
-    v = ev ? atoi(ev) : 1;
-    if (v < 1) v = 1;
-    if (v > 8) v = 8;
-  }
+  static const int v = [] {
+    const int e = env_int("RNT_KS_SPLIT", 1);
+    return e < 1 ? 1 : (e > 8 ? 8 : e);
+  }();
   return (uint32_t)v < dnum ? (uint32_t)v : dnum;
 }
 
@@ -646,11 +637,8 @@ static rnt_status ks_fused_launch(const rnt_plan_s* qp, u64* u, u64* E, const u6
   }
   constexpr int RPC = P::RPC;
   const size_t smem = (size_t)2 * RPC * P::Cn * 8;
-  static bool attr_set = false;  // benign race: idempotent attribute call
-  if (!attr_set) {
-    RNT_CUDA(cudaFuncSetAttribute(k_row_mac<LOGN, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (rnt_status s = ensure_attr(k_row_mac<LOGN, RPC>, smem, attr); s != RNT_OK) return s;
   dim3 g(P::R / RPC, LK, split);
   k_row_mac<LOGN, RPC><<<g, RPC * P::T2, smem, st>>>(u, E, evk, qp->d_fwd, qp->d_lc, LK, dnum, split);
   rnt_status s = after_launch();
@@ -875,12 +863,10 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   // pays each kernel's ramp and tail three times; running G limb windows as
   // independent kernel chains on G streams lets the windows overlap
   // (measured: 2^16 x 45 limbs polymul 0.103 -> 0.094 ms with G = 2).
-  static int split_g = -1;
-  if (split_g < 0) {
-    const char* ev = getenv("RNT_SPLIT");
-    split_g = ev ? atoi(ev) : 2;
-    if (split_g > 4) split_g = 4;
-  }
+  static const int split_g = [] {
+    const int v = env_int("RNT_SPLIT", 2);
+    return v > 4 ? 4 : v;
+  }();
   if (split_g > 1 && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
     std::lock_guard<std::mutex> g(p->split_mu);
     for (int i = 0; i < split_g; ++i)
@@ -1018,11 +1004,7 @@ rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint3
   if (e != cudaSuccess) return cuda_fail(e);
   if (d != c->device) return RNT_E_PLAN_MISMATCH;
   const size_t smem = (size_t)c->L * kBcTile * 8;
-  static size_t attr = 0;  // benign race: idempotent attribute call
-  if (smem > 48 * 1024 && attr < smem) {
-    RNT_CUDA(cudaFuncSetAttribute(k_bconv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  if (rnt_status s = set_smem(k_bconv, smem); s != RNT_OK) return s;
   const uint32_t n = 1u << c->logn;
   dim3 grid((n + kBcTile - 1) / kBcTile, batch);
   k_bconv<<<grid, kBcTile, smem, (cudaStream_t)stream>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in),
@@ -1113,11 +1095,7 @@ rnt_status rnt_keyswitch_create(rnt_keyswitch* out, rnt_plan q_plan, rnt_plan qp
     uint64_t qmax = 0, mmin = ~0ull;
     for (uint32_t i = 0; i < L; ++i) qmax = m[i] > qmax ? m[i] : qmax;
     for (uint32_t t = 0; t < LK; ++t) mmin = m[t] < mmin ? m[t] : mmin;
-    static int force_unfused = -1;
-    if (force_unfused < 0) {
-      const char* ev = getenv("RNT_KS_UNFUSED");
-      force_unfused = ev && atoi(ev) > 0;
-    }
+    static const bool force_unfused = env_int("RNT_KS_UNFUSED", 0) > 0;
     ks->fused = !force_unfused && ks->logn >= 11 && alpha == 1 && qmax / 2 < mmin;
     ks->split = ks->fused ? ks_split(dnum) : 1;
   }
@@ -1184,11 +1162,7 @@ rnt_status rnt_keyswitch_apply(rnt_keyswitch ks, uint64_t* out_, const uint64_t*
   // 2. ModUp every digit, then NTT of the extended polynomials (batch = dnum)
   {
     const size_t smem = (size_t)ks->alpha * kKsTile * 8;
-    static size_t attr = 0;  // benign race: idempotent attribute call
-    if (smem > 48 * 1024 && attr < smem) {
-      RNT_CUDA(cudaFuncSetAttribute(k_modup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    if ((s = set_smem(k_modup, smem)) != RNT_OK) return s;
     dim3 grid((unsigned)((n + kKsTile - 1) / kKsTile), ks->dnum);
     k_modup<<<grid, kKsTile, smem, st>>>(E, x, ks->d_km, ks->d_tab, L, LK, ks->alpha, logn);
     if ((s = after_launch()) != RNT_OK) return s;
@@ -1212,11 +1186,7 @@ rnt_status rnt_keyswitch_apply(rnt_keyswitch ks, uint64_t* out_, const uint64_t*
       if ((s = run_op(&pv, 1, U(up + (size_t)k * K * n), U(u + ((size_t)k * LK + L) * n), nullptr, 0, 1, st)) != RNT_OK)
         return s;
     const size_t smem = (size_t)K * kBcTile * 8;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-      RNT_CUDA(cudaFuncSetAttribute(k_bconv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    if ((s = set_smem(k_bconv, smem)) != RNT_OK) return s;
     dim3 grid((unsigned)((n + kBcTile - 1) / kBcTile), 2);
     k_bconv<<<grid, kBcTile, smem, st>>>(w, up, ks->d_bsrc, ks->d_bdst, ks->d_bqp, K, L, logn);
     if ((s = after_launch()) != RNT_OK) return s;
@@ -1290,19 +1260,12 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   // Chunking: chunks over polynomials (batch > 1) or limbs (batch == 1),
   // round-robin over three internal streams so H2D copy, kernels and D2H copy
   // of successive chunks overlap.  Fork/join with the caller's stream by events.
-  static size_t target = 0;  // chunk bytes (tuning knob RNT_CHUNK_MB, default 16 MiB, measured best)
-  if (!target) {
-    const char* ev = getenv("RNT_CHUNK_MB");
-    target = (size_t)(ev && atoi(ev) > 0 ? atoi(ev) : 16) << 20;
-  }
+  // chunk bytes (tuning knob RNT_CHUNK_MB, default 16 MiB, measured best)
+  static const size_t target = (size_t)(env_int("RNT_CHUNK_MB", 16) > 0 ? env_int("RNT_CHUNK_MB", 16) : 16) << 20;
   // Granule = one polynomial (batch > 1) or one limb (batch == 1).  Chunks of
   // `target` bytes, except that the first and last chunks ramp (target/8,
   // /4, /2, ...) so the copy engines start and drain sooner (env RNT_CHUNK_RAMP=0: uniform).
-  static int ramp = -1;
-  if (ramp < 0) {
-    const char* ev = getenv("RNT_CHUNK_RAMP");
-    ramp = ev ? atoi(ev) > 0 : 1;
-  }
+  static const bool ramp = env_int("RNT_CHUNK_RAMP", 1) > 0;
   const size_t gbytes = batch > 1 ? (size_t)p->L * unit_bytes : unit_bytes;
   const size_t G = batch > 1 ? batch : p->L;
   size_t T = target / gbytes;
