@@ -303,9 +303,43 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 
+// Latency engine (k_lat, ntt_small.cuh) for jobs of at most lat_units()
+// (polynomial, limb) units at N <= 2^10 (env RNT_LAT_UNITS; 0 disables).  Default
+// 512: measured crossover with the warp engine near 1024 units (2^10 polymul,
+// 18.6 vs 24.7 us at 512 units, 52.5 vs 46.6 us at 2048).
+static int lat_units() {
+  static const int v = env_int("RNT_LAT_UNITS", 512);
+  return v;
+}
+
+template <int LOGN, int MODE>
+static rnt_status launch_lat(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast, uint32_t batch,
+                             cudaStream_t st) {
+  const uint64_t units = (uint64_t)batch * p->L;
+  k_lat<LOGN, MODE><<<(unsigned)units, (1 << LOGN) / 2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_inv, p->d_lc,
+                                                                   p->L);
+  return after_launch();
+}
+
+template <int MODE>
+static rnt_status lat_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                               uint32_t batch, cudaStream_t st) {
+  switch (p->logn) {
+    case 4: return launch_lat<4, MODE>(p, out, in, bop, bcast, batch, st);
+    case 5: return launch_lat<5, MODE>(p, out, in, bop, bcast, batch, st);
+    case 6: return launch_lat<6, MODE>(p, out, in, bop, bcast, batch, st);
+    case 7: return launch_lat<7, MODE>(p, out, in, bop, bcast, batch, st);
+    case 8: return launch_lat<8, MODE>(p, out, in, bop, bcast, batch, st);
+    case 9: return launch_lat<9, MODE>(p, out, in, bop, bcast, batch, st);
+    case 10: return launch_lat<10, MODE>(p, out, in, bop, bcast, batch, st);
+    default: return RNT_E_UNSUPPORTED_N;
+  }
+}
+
 template <int MODE>
 static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                 uint32_t batch, cudaStream_t st) {
+  if ((uint64_t)batch * p->L <= (uint64_t)lat_units()) return lat_dispatch<MODE>(p, out, in, bop, bcast, batch, st);
   switch (p->logn) {
     case 4: return launch_warp<4, MODE>(p, out, in, bop, bcast, batch, st);
     case 5: return launch_warp<5, MODE>(p, out, in, bop, bcast, batch, st);

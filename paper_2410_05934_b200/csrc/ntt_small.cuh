@@ -640,3 +640,111 @@ inline size_t warp_smem_bytes() {
 }
 
 }  // namespace rnt
+
+// ============================ latency engine =================================
+// One CTA of N/2 threads per (polynomial, limb) unit, one butterfly per thread
+// per stage, the polynomial in shared memory, a CTA barrier between stages:
+// the loops of Eq. 1 exactly as written (Longa-Naehrig CT forward, GS inverse,
+// P:205-213) with the Shoup butterflies of modarith.cuh.  For latency-bound
+// jobs (a handful of units, e.g. cfg1's single polynomial), where the warp
+// engine would leave one warp doing all N/2 log N butterflies alone.
+// MODE 0 forward, 1 inverse, 2 c = INTT(NTT(a) (.) b_hat), 3 c = INTT(NTT(a) (.) NTT(b)).
+namespace rnt {
+
+template <int LOGN>
+__device__ __forceinline__ void lat_forward(u64* a, const TW* F, u64 q, u64 q2) {   // F: shared-memory table
+  constexpr int N = 1 << LOGN;
+  const int b = threadIdx.x;
+#pragma unroll 1
+  for (int m = 1, lt = LOGN - 1; m < N; m <<= 1, --lt) {   // t = 2^lt = N / (2m)
+    const int t = 1 << lt;
+    const int i = b >> lt, j = 2 * i * t + (b & (t - 1));
+    u64 X = a[j], Y = a[j + t];
+    ct_bfly(X, Y, F[m + i], q, q2);
+    a[j] = X;
+    a[j + t] = Y;
+    __syncthreads();
+  }
+}
+
+template <int LOGN, bool AFTER_MONT>
+__device__ __forceinline__ void lat_inverse(u64* a, const TW* I, const LimbC& c, u64 q, u64 q2) {
+  constexpr int N = 1 << LOGN;
+  const int b = threadIdx.x;
+#pragma unroll 1
+  for (int h = N / 2, lt = 0; h > 1; h >>= 1, ++lt) {       // t = 2^lt, twiddle inv[h + i]
+    const int t = 1 << lt;
+    const int i = b >> lt, j = 2 * i * t + (b & (t - 1));
+    u64 X = a[j], Y = a[j + t];
+    gs_bfly(X, Y, I[h + i], q, q2);
+    a[j] = X;
+    a[j + t] = Y;
+    __syncthreads();
+  }
+  // last stage (h = 1, t = N/2) with the N^{-1} scale folded in (reading C4 / C15)
+  u64 X = a[b], Y = a[b + N / 2];
+  gs_bfly_last(X, Y, AFTER_MONT ? c.ninvR : c.ninv, AFTER_MONT ? c.ninvR_w1 : c.ninv_w1, q, q2);
+  a[b] = canon2(X, q);
+  a[b + N / 2] = canon2(Y, q);
+}
+
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__((1 << LOGN) / 2)
+k_lat(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
+      const TW* __restrict__ fwd, const TW* __restrict__ inv, const LimbC* __restrict__ lc, uint32_t L) {
+  constexpr int N = 1 << LOGN, H = N / 2;
+  __shared__ __align__(16) u64 a[N];
+  __shared__ __align__(16) u64 bb[MODE == 3 ? N : 1];
+  // twiddle tables staged once in shared memory (every stage then reads shared
+  // memory, not L2); MODE 3 reuses the forward table's space for the inverse one
+  __shared__ __align__(16) TW F[MODE != 1 ? N : 1];
+  __shared__ __align__(16) TW Ibuf[(MODE == 1 || MODE == 2) ? N : 1];
+  TW* I = MODE == 3 ? F : Ibuf;
+  const uint64_t u = blockIdx.x;
+  const uint32_t l = (uint32_t)(u % L);
+  const LimbC c = lc[l];
+  const u64 q = c.q, q2 = c.q2;
+  const int b = threadIdx.x;
+  if constexpr (MODE != 1) {
+    F[b] = ldg_tw(fwd + ((size_t)l << LOGN) + b);
+    F[b + H] = ldg_tw(fwd + ((size_t)l << LOGN) + b + H);
+  }
+  if constexpr (MODE == 1 || MODE == 2) {
+    I[b] = ldg_tw(inv + ((size_t)l << LOGN) + b);
+    I[b + H] = ldg_tw(inv + ((size_t)l << LOGN) + b + H);
+  }
+  const u64* src = in + (u << LOGN);
+  a[b] = src[b];
+  a[b + H] = src[b + H];
+  const u64* bsrc = bop ? bop + ((b_bcast ? (uint64_t)l : u) << LOGN) : nullptr;
+  if constexpr (MODE == 3) {
+    bb[b] = bsrc[b];
+    bb[b + H] = bsrc[b + H];
+  }
+  __syncthreads();
+  if constexpr (MODE != 1) lat_forward<LOGN>(a, F, q, q2);
+  if constexpr (MODE == 3) {
+    lat_forward<LOGN>(bb, F, q, q2);   // ends with a barrier: F is free
+    I[b] = ldg_tw(inv + ((size_t)l << LOGN) + b);
+    I[b + H] = ldg_tw(inv + ((size_t)l << LOGN) + b + H);
+  }
+  u64* dst = out + (u << LOGN);
+  if constexpr (MODE == 0) {
+    dst[b] = canon4(a[b], q, q2);
+    dst[b + H] = canon4(a[b + H], q, q2);
+    return;
+  } else {
+    if constexpr (MODE >= 2) {
+      const u64 b0 = MODE == 3 ? canon4(bb[b], q, q2) : __ldg(bsrc + b);
+      const u64 b1 = MODE == 3 ? canon4(bb[b + H], q, q2) : __ldg(bsrc + b + H);
+      a[b] = mont_mul(a[b], b0, q, c.qinv);
+      a[b + H] = mont_mul(a[b + H], b1, q, c.qinv);
+      __syncthreads();
+    }
+    lat_inverse<LOGN, (MODE >= 2)>(a, I, c, q, q2);
+    dst[b] = a[b];
+    dst[b + H] = a[b + H];
+  }
+}
+
+}  // namespace rnt

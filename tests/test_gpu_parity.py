@@ -339,6 +339,36 @@ def test_limb_split_single_poly(logn, limbs, op):
     assert np.array_equal(from_dev(d), want)
 
 
+@pytest.mark.parametrize("logn", [4, 5, 7, 9, 10])
+@pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 3), (1, 8)])
+@pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul", "polymul_bcast"])
+def test_latency_path(logn, limbs, batch, op):
+    """batch * L <= 8 at N <= 2^10 runs the latency engine k_lat (one CTA per unit)."""
+    ps, psi = params(logn, limbs)
+    p = R.Plan(logn, ps)
+    n = 1 << logn
+    a = inputs.residues(51 + logn, batch, ps, n)
+    bc = op == "polymul_bcast"
+    b = inputs.residues(52 + logn, 1 if bc else batch, ps, n)
+    d = empty_dev(a.shape)
+    n0 = R.launch_count()
+    if op == "fwd":
+        R.ntt_forward(p, d, to_dev(a))
+        want = O.batch(O.OP_FWD, a, ps, psi)
+    elif op == "inv":
+        R.ntt_inverse(p, d, to_dev(a))
+        want = O.batch(O.OP_INV, a, ps, psi)
+    elif op == "polymul_eval":
+        bh = O.batch(O.OP_FWD, b, ps, psi)
+        R.polymul(p, d, to_dev(a), to_dev(bh), b_is_eval=True)
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b)
+    else:
+        R.polymul(p, d, to_dev(a), to_dev(b), b_broadcast=bc)
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, b_broadcast=bc)
+    assert R.launch_count() - n0 == 1
+    assert np.array_equal(from_dev(d), want)
+
+
 @pytest.mark.parametrize("logn", [11, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 1), (1, 2)])
 @pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_bcast"])
@@ -392,7 +422,8 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
                          [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)] +
                          [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)] +
                          [{"RNT_CLUSTER_C": "8"}, {"RNT_CLUSTER_C": "16"}, {"RNT_CLUSTER_UNITS": "0"},
-                          {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"}])
+                          {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"},
+                          {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""

@@ -22,6 +22,7 @@ KEYS = {
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "fmaheavy_pipe_pct": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
     "inst_executed": "smsp__inst_executed.sum",
     "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -58,6 +59,10 @@ def scale(val, unit, want):
     return val
 
 
+def fmt(v):
+    return "-" if v is None else f"{v:.0f}"
+
+
 def main():
     prefix, reps = sys.argv[1], sys.argv[2:]
     allk = []
@@ -84,13 +89,13 @@ def main():
             allk.append(k)
     json.dump(allk, open(prefix + ".json", "w"), indent=1)
     with open(prefix + ".md", "w") as f:
-        f.write("| kernel | us | DRAM R/W MB | regs | warps act % | issue % | fma pipe % | alu pipe % | top stalls (cycles/issue) |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|\n")
+        f.write("| kernel | us | DRAM R/W MB | regs | warps act % | issue % | fma pipe % | fmaheavy % | alu pipe % | top stalls (cycles/issue) |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|\n")
         for k in allk:
             st = ", ".join(f"{a} {b}" for a, b in list(k["stalls_per_issue"].items())[:5])
             f.write(f"| {k['kernel'][:48]} | {k['duration_us']:.1f} | {k['dram_read_MB']:.1f}/{k['dram_write_MB']:.1f} | "
                     f"{k['regs']:.0f} | {k['warps_active_pct']:.0f} | {k['issue_active_pct']:.0f} | "
-                    f"{k['fma_pipe_pct']:.0f} | {k['alu_pipe_pct']:.0f} | {st} |\n")
+                    f"{k['fma_pipe_pct']:.0f} | {fmt(k.get('fmaheavy_pipe_pct'))} | {k['alu_pipe_pct']:.0f} | {st} |\n")
     print(open(prefix + ".md").read())
 
 
