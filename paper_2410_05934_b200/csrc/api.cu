@@ -43,6 +43,7 @@ struct rnt_plan_s {
   cudaStream_t split[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t split_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   bool is_view = false;     // limb-window view used internally (owns nothing)
+  bool lazy60 = false;      // every modulus < 2^60: LZ kernels (ct_bfly_lz, 16q lazy bound) are valid
 };
 
 // Shallow limb-window view [l0, l0 + nl) of a plan (for batch == 1 chunking).
@@ -61,6 +62,7 @@ static void make_view(const rnt_plan_s* p, uint32_t l0, uint32_t nl, rnt_plan_s*
     v->d_rowtw = p->d_rowtw + l0 * n;
   }
   v->is_view = true;
+  v->lazy60 = p->lazy60;
 }
 
 static thread_local int g_last_cuda = 0;
@@ -224,18 +226,18 @@ static rnt_status set_smem(K kern, size_t smem) {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4>
+template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
-  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM>, smem, attr); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ>, smem, attr); s != RNT_OK) return s;
   const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    k_warp<LOGN, MODE, W, MINB, SYNC, KM><<<grid, W * 32, smem, st>>>(
+    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ><<<grid, W * 32, smem, st>>>(
         out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
         p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
@@ -248,6 +250,11 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
 // configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
 static int small_variant() {
   static const int v = env_int("RNT_SMALL_VARIANT", 0);
+  return v;
+}
+
+static bool lazy_enabled() {
+  static const bool v = env_int("RNT_LAZY", 1) != 0;
   return v;
 }
 
@@ -299,7 +306,9 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
     }
   }
   // default: radix-8 passes (N=2^10: 3+3+3+1), 2 warps per CTA, <= 85 registers
-  // (24 warps/SM) -- fastest measured (profiles/r01/README.md)
+  // (24 warps/SM) -- fastest measured (profiles/r01/README.md); lazy CT ranges
+  // when every modulus is below 2^60 (env RNT_LAZY=0 disables)
+  if (p->lazy60 && lazy_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
   return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 
@@ -766,6 +775,8 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   const uint32_t n1 = (log2n + 1) / 2;
   const bool large = log2n > 10;
 
+  p->lazy60 = true;
+  for (uint32_t l = 0; l < n_limbs; ++l) p->lazy60 = p->lazy60 && limbs[l].q < (1ull << 60);
   std::vector<LimbC> lc(n_limbs);
   for (uint32_t l = 0; l < n_limbs; ++l) {
     const HostLimb& h = limbs[l];

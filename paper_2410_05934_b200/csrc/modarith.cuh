@@ -81,6 +81,19 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
   Y = shoup_lazy(d, t, q);      // [0, 2q)
 }
 
+// CT butterfly without the input reduction, for moduli q < 2^60 (16 q < 2^64;
+// LZ kernels, plan flag lazy60): X in [0, B q) -> X' , Y' in [0, (B + 2) q).
+// Starting from canonical input, stages 0..6 need no reduction (bound 15 q);
+// at stage 7 (RED) X is reduced by 8q ([0, 15q) -> [0, 8q)), so 2^10-point
+// outputs stay below 14 q.  Saves the csub of 9 out of 10 stages.
+template <bool RED>
+__device__ __forceinline__ void ct_bfly_lz(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  u64 x = RED ? csub(X, q2 << 2) : X;
+  u64 v = shoup_lazy(Y, t, q);  // [0, 2q)
+  X = x + v;
+  Y = x + q2 - v;
+}
+
 // GS butterfly with a negated twiddle: (X, Y) -> (X + Y, (Y - X) w).  With
 // w = psi^{brv(k')} of the mirrored index k' = 3 2^s - 1 - k this equals the GS
 // butterfly with psi^{-brv(k)} = -psi^{brv(k')}, so inverse row stages can read
@@ -103,6 +116,10 @@ __device__ __forceinline__ void gs_bfly_last(u64& X, u64& Y, TW s0, TW s1, u64 q
 
 // [0, 4q) -> [0, q)
 __device__ __forceinline__ u64 canon4(u64 x, u64 q, u64 q2) { return csub(csub(x, q2), q); }
+// [0, 16q) -> [0, q) (LZ outputs)
+__device__ __forceinline__ u64 canon16(u64 x, u64 q, u64 q2) {
+  return csub(csub(csub(csub(x, q2 << 2), q2 << 1), q2), q);
+}
 // [0, 2q) -> [0, q)
 __device__ __forceinline__ u64 canon2(u64 x, u64 q) { return csub(x, q); }
 

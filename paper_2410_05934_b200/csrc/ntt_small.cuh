@@ -75,7 +75,8 @@ struct PassGeo {
 };
 
 // K CT stages on x[0 .. 2^K) of one group; twiddle w[2^{S+v} + hi 2^v + blk].
-template <int S, int K>
+// LZ: lazy ranges for q < 2^60 (ct_bfly_lz; input canonical at stage 0).
+template <int S, int K, bool LZ = false>
 __device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, u64 q, u64 q2) {
   sfor<0, K>([&](auto V_) {
     constexpr int v = decltype(V_)::value;
@@ -84,9 +85,21 @@ __device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, 
     for (int blk = 0; blk < (1 << v); ++blk) {
       TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
 #pragma unroll
-      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      for (int k = 0; k < half; ++k) {
+        if constexpr (LZ)
+          ct_bfly_lz<S + v == 7>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+        else
+          ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      }
     }
   });
+}
+
+// canonical value of a forward output (lazy bound 4q, or 16q with LZ)
+template <bool LZ>
+__device__ __forceinline__ u64 canon_fwd(u64 x, u64 q, u64 q2) {
+  if constexpr (LZ) return canon16(x, q, q2);
+  else return canon4(x, q, q2);
 }
 
 // K GS stages (reverse order).  If LAST (S == 0), local stage 0 is the final
@@ -141,7 +154,7 @@ constexpr int kToBufCanon = 2; // canonical values into the warp buffer
 // ---- one forward pass (CT) over the warp buffer -----------------------------
 // TWS: twiddle-table stride per polynomial of the warp (0: all polynomials
 // share T; 2^{n2}: row r + p of a 2^16 limb uses row table r + p).
-template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0>
+template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false>
 __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2,
                                          const u64* raw = nullptr) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -164,17 +177,17 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
-    ct_group<S, K>(x, T + g.poly * TWS, g.hi, q, q2);
+    ct_group<S, K, LZ>(x, T + g.poly * TWS, g.hi, q, q2);
     if constexpr (DST == kToGlobal) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
 #pragma unroll
-        for (int i = 0; i < (1 << K); ++i) d[i * Geo::LO] = canon4(x[i], q, q2);
+        for (int i = 0; i < (1 << K); ++i) d[i * Geo::LO] = canon_fwd<LZ>(x[i], q, q2);
       }
     } else {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i)
-        buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = DST == kToBufCanon ? canon4(x[i], q, q2) : x[i];
+        buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = DST == kToBufCanon ? canon_fwd<LZ>(x[i], q, q2) : x[i];
     }
   }
   __syncwarp();
@@ -222,7 +235,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 // GS pass, all in registers.  b_hat comes from global memory (bview) or from
 // a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf), or a TMA-staged raw buffer (kFromRaw).
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC, bool SCALE = true, int TWS = 0,
-          bool MIRROR = false>
+          bool MIRROR = false, bool LZ = false>
 __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                           const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv,
                                           const u64* raw = nullptr, const u64* braw = nullptr) {
@@ -260,7 +273,8 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) bv[i] = live ? __ldg(b + i * Geo::LO) : 0ull;
     }
-    ct_group<S, K>(x, Tf + g.poly * TWS, g.hi, q, q2);
+    ct_group<S, K, LZ>(x, Tf + g.poly * TWS, g.hi, q, q2);
+    // a < 16q (LZ, q < 2^60) or < 4q, b_hat < q: a b < q 2^64, result in (0, 2q)
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bv[i], q, qinv);
     gs_group<S, K, SCALE && S == 0, MIRROR>(x, MIRROR ? Ti - g.poly * TWS : Ti + g.poly * TWS, g.hi, s0, s1, q, q2);
@@ -288,14 +302,14 @@ struct Passes {
   __host__ __device__ static constexpr int s(int p) { return p * KM; }
 };
 
-template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0>
+template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
     constexpr int SRC = p == 0 ? kFromGlobal : kFromBuf;
     constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
@@ -314,17 +328,20 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
   });
 }
 
-template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false>
+template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false,
+          bool LZ = false>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using PS = Passes<LOGN, KM>;
   constexpr int NP = PS::NP;
   sfor<0, NP - 1>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS>(buf, src, dst, lane, Tf, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS, LZ>(buf, src, dst, lane, Tf, q,
+                                                                                        q2);
     if constexpr (SYNC) __syncthreads();
   });
-  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR>(
+  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR,
+            LZ>(
       buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
   if constexpr (SYNC) __syncthreads();
   sfor<0, NP - 1>([&](auto I_) {
@@ -340,7 +357,8 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
-template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4>
+// LZ: lazy CT ranges (ct_bfly_lz), valid when every modulus of the plan is < 2^60.
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false>
 __global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
@@ -361,7 +379,7 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Tf = tw_fwd + (size_t)l * N;
   const TW* Ti = tw_inv + (size_t)l * N;
   if constexpr (MODE == 0) {
-    warp_forward<LOGN, KM, kToGlobal, SYNC>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
     warp_inverse<LOGN, KM, SYNC>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
   } else {
@@ -370,10 +388,10 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
     if constexpr (MODE == 3) {
       u64* bbuf = buf + kWarpBuf;
       // canonical NTT(b) parked in the second warp buffer
-      warp_forward<LOGN, KM, kToBufCanon, SYNC>(bbuf, bview, bview, lane, Tf, q, q2);
-      warp_polymul<LOGN, KM, kFromBuf, SYNC>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+      warp_forward<LOGN, KM, kToBufCanon, SYNC, 0, LZ>(bbuf, bview, bview, lane, Tf, q, q2);
+      warp_polymul<LOGN, KM, kFromBuf, SYNC, true, 0, false, LZ>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     } else {
-      warp_polymul<LOGN, KM, kFromGlobal, SYNC>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
+      warp_polymul<LOGN, KM, kFromGlobal, SYNC, true, 0, false, LZ>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
                                 qinv);
     }
   }

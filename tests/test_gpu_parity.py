@@ -423,7 +423,8 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
                          [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)] +
                          [{"RNT_CLUSTER_C": "8"}, {"RNT_CLUSTER_C": "16"}, {"RNT_CLUSTER_UNITS": "0"},
                           {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"},
-                          {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"}])
+                          {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"},
+                          {"RNT_LAZY": "0", "RNT_LAT_UNITS": "0"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
@@ -586,3 +587,48 @@ def test_debug_range_validation():
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RNT_DEBUG": "1"}, capture_output=True,
                        text=True, timeout=600)
     assert "DEBUG_OK" in r.stdout, r.stdout + r.stderr
+
+
+def _primes_below(bits, logn, count):
+    """q = 1 (mod 2N) descending from 2^bits (primality from the oracle)."""
+    two_n = 2 << logn
+    k, out = ((1 << bits) - 1) // two_n, []
+    while len(out) < count:
+        if O.is_prime(k * two_n + 1):
+            out.append(k * two_n + 1)
+        k -= 1
+    return out
+
+
+@pytest.mark.parametrize("logn", [4, 7, 8, 10])
+@pytest.mark.parametrize("bits", [60, 62])
+def test_warp_engine_lazy_ranges(logn, bits):
+    """The batched warp engine (k_warp, > 512 units) at the extremes of its lazy
+    ranges: 60-bit moduli take the LZ kernels (no CT reduction until stage 7,
+    16q bound), moduli in [2^61, 2^62) the Harvey [0, 4q) kernels.  Inputs mix
+    all-(q-1), alternating 0 / q-1, deltas and random residues."""
+    n = 1 << logn
+    ps = _primes_below(bits, logn, 1)
+    psi = [O.min_psi(q, logn) for q in ps]
+    p = R.Plan(logn, ps)
+    q = ps[0]
+    B = 640
+    a = inputs.residues(77 + logn, B, ps, n)
+    a[0::4, 0, :] = q - 1
+    a[1::8, 0, :] = np.array([0 if i % 2 else q - 1 for i in range(n)], dtype=np.uint64)
+    a[3::8, 0, :] = 0
+    a[3::8, 0, 0] = 1
+    b = inputs.residues(88 + logn, B, ps, n)
+    b[0::3, 0, :] = q - 1
+    want = O.batch(O.OP_FWD, a, ps, psi, n_threads=8)
+    d = empty_dev(a.shape)
+    R.ntt_forward(p, d, to_dev(a))
+    assert np.array_equal(from_dev(d), want)
+    R.ntt_inverse(p, d, to_dev(want))
+    assert np.array_equal(from_dev(d), a)
+    bhat = O.batch(O.OP_FWD, b, ps, psi, n_threads=8)
+    bhat[1::5, 0, :] = q - 1
+    R.polymul(p, d, to_dev(a), to_dev(bhat), b_is_eval=True)
+    assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bhat, n_threads=8))
+    R.polymul(p, d, to_dev(a), to_dev(b), b_is_eval=False)
+    assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8))
