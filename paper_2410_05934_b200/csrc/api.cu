@@ -378,7 +378,7 @@ static int large_variant() {
   return v >= 0 ? v : g_large_auto;
 }
 
-template <int LOGN, int CT>
+template <int LOGN, int CT, bool LZ = false>
 static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
                                uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
@@ -389,7 +389,7 @@ static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u6
     if (inv)
       k_col_inv<LOGN, CT><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_inv, p->d_lc, p->L, batch, y0, after_mont);
     else
-      k_col_fwd<LOGN, CT><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
+      k_col_fwd<LOGN, CT, false, LZ><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -399,11 +399,17 @@ static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u6
 template <int LOGN>
 static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
                              uint32_t batch, cudaStream_t st) {
+  // forward columns with lazy CT ranges when the plan allows it; the row pass
+  // that consumes them (launch_row) makes the same choice
+  if (!inv && p->lazy60 && lazy_enabled()) {
+    if (large_variant() & 1) return launch_col_v<LOGN, 8, true>(p, inv, after_mont, out, in, batch, st);
+    return launch_col_v<LOGN, kColTile, true>(p, inv, after_mont, out, in, batch, st);
+  }
   if (large_variant() & 1) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
   return launch_col_v<LOGN, kColTile>(p, inv, after_mont, out, in, batch, st);
 }
 
-template <int LOGN, int MODE, int RPC_>
+template <int LOGN, int MODE, int RPC_, bool LZ = false>
 static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
@@ -411,27 +417,27 @@ static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, con
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(P::R / RPC_, (unsigned)cnt);
-    k_row<LOGN, MODE, RPC_><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_lc, p->L, batch, y0);
+    k_row<LOGN, MODE, RPC_, LZ><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
   return RNT_OK;
 }
 
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, bool LZ = false>
 static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                    uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
   static std::atomic<uint64_t> attr{0};
   const size_t smem = (size_t)kRowWarps * kWarpBuf * 8;
-  if (rnt_status s = ensure_attr(k_rows<LOGN, MODE>, smem, attr); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(k_rows<LOGN, MODE, LZ>, smem, attr); s != RNT_OK) return s;
   constexpr int rows_per_cta = kRowWarps * (kWarpElems / P::Cn);
   const unsigned gx = (unsigned)((P::R + rows_per_cta - 1) / rows_per_cta);
   const uint64_t units = (uint64_t)batch * p->L;
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(gx, (unsigned)cnt);
-    k_rows<LOGN, MODE><<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
+    k_rows<LOGN, MODE, LZ><<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -441,8 +447,16 @@ static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in,
 template <int LOGN, int MODE>
 static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                              uint32_t batch, cudaStream_t st) {
-  if (large_variant() & 4) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
   constexpr int R4 = TwoPass<LOGN>::RPC / 4 > 0 ? TwoPass<LOGN>::RPC / 4 : 1;
+  if constexpr (MODE != 1) {
+    // input from an LZ forward column pass (launch_col makes the same choice)
+    if (p->lazy60 && lazy_enabled()) {
+      if (large_variant() & 4) return launch_rows_warp<LOGN, MODE, true>(p, out, in, bop, bcast, batch, st);
+      if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4, true>(p, out, in, bop, bcast, batch, st);
+      return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC, true>(p, out, in, bop, bcast, batch, st);
+    }
+  }
+  if (large_variant() & 4) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
   if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4>(p, out, in, bop, bcast, batch, st);
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }

@@ -82,16 +82,32 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
 }
 
 // CT butterfly without the input reduction, for moduli q < 2^60 (16 q < 2^64;
-// LZ kernels, plan flag lazy60): X in [0, B q) -> X' , Y' in [0, (B + 2) q).
-// Starting from canonical input, stages 0..6 need no reduction (bound 15 q);
-// at stage 7 (RED) X is reduced by 8q ([0, 15q) -> [0, 8q)), so 2^10-point
-// outputs stay below 14 q.  Saves the csub of 9 out of 10 stages.
+// LZ kernels, plan flag lazy60): X in [0, B q) -> X', Y' in [0, (B + 2) q).
+// From canonical input at global stage 0 the bound grows by 2q per stage and
+// X is reduced by 8q only when the bound would pass 16q (RED: [0, 16q) ->
+// [0, 8q)): stages 7, 11, 15 of a 2^16 transform, only stage 7 at 2^10, so
+// 13 of 16 (9 of 10) stages drop the csub of Harvey's butterfly.
+__host__ __device__ constexpr int lz_bound_before(int s) {
+  int b = 1;
+  for (int i = 0; i < s; ++i) b = (b > 14 ? 8 : b) + 2;
+  return b;
+}
+__host__ __device__ constexpr bool lz_red(int s) { return lz_bound_before(s) > 14; }
+static_assert(lz_bound_before(7) == 15 && lz_red(7) && !lz_red(6) && lz_red(11) && lz_red(15), "LZ schedule");
+
 template <bool RED>
 __device__ __forceinline__ void ct_bfly_lz(u64& X, u64& Y, TW t, u64 q, u64 q2) {
   u64 x = RED ? csub(X, q2 << 2) : X;
   u64 v = shoup_lazy(Y, t, q);  // [0, 2q)
   X = x + v;
   Y = x + q2 - v;
+}
+
+// CT butterfly of global stage s: Harvey's [0, 4q) form, or the LZ form.
+template <bool LZ, int s>
+__device__ __forceinline__ void ct_bfly_at(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  if constexpr (LZ) ct_bfly_lz<lz_red(s)>(X, Y, t, q, q2);
+  else ct_bfly(X, Y, t, q, q2);
 }
 
 // GS butterfly with a negated twiddle: (X, Y) -> (X + Y, (Y - X) w).  With

@@ -56,7 +56,9 @@ __device__ __forceinline__ int row_swz(int c) {
 // MODUP (key switching, keyswitch.cuh): unit (poly j, limb t) reads limb j of a
 // single L-limb polynomial (one-prime digits, reading KS2 with alpha = 1) and
 // lifts it to q_t on load: x mod q_t = x - q_t if x >= q_t (requires q_j < 2 q_t).
-template <int LOGN, int CT = kColTile, bool MODUP = false>
+// LZ: lazy CT ranges (modarith.cuh ct_bfly_lz, plan flag lazy60); the output
+// then carries the LZ bound of stage n1 and must feed an LZ row pass.
+template <int LOGN, int CT = kColTile, bool MODUP = false, bool LZ = false>
 __global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
 k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
@@ -87,7 +89,8 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
     for (int blk = 0; blk < (1 << s); ++blk) {
       TW w = ldg_tw(T + (1 << s) + blk);
 #pragma unroll
-      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      for (int k = 0; k < half; ++k)
+        ct_bfly_at<LZ, s>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
     }
   });
 #pragma unroll
@@ -104,7 +107,7 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
     for (int m = 0; m < kEl / (2 * t); ++m) {
       TW w = ldg_tw(T + (1 << s) + ((kEl * r1 + m * 2 * t) >> (P::n1 - s)));
 #pragma unroll
-      for (int k = 0; k < t; ++k) ct_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+      for (int k = 0; k < t; ++k) ct_bfly_at<LZ, s>(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
     }
   });
 #pragma unroll
@@ -169,7 +172,7 @@ k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
 // w[2^{n1+v} + r 2^v + k]; for v >= 4 entry m*T2 + c1 holds
 // w[2^{n1+v} + r 2^v + c1 2^{v+4-n2} + m] (lane-major: coalesced loads).
 
-template <int LOGN>
+template <int LOGN, bool LZ = false>
 __device__ __forceinline__ void row_fwd_A(u64 (&x)[kEl], const TW* Tr, u64 q, u64 q2) {
   sfor<0, 4>([&](auto V_) {
     constexpr int v = decltype(V_)::value;
@@ -178,12 +181,13 @@ __device__ __forceinline__ void row_fwd_A(u64 (&x)[kEl], const TW* Tr, u64 q, u6
     for (int blk = 0; blk < (1 << v); ++blk) {
       TW w = ldg_tw(Tr + (1 << v) - 1 + blk);
 #pragma unroll
-      for (int k = 0; k < half; ++k) ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      for (int k = 0; k < half; ++k)
+        ct_bfly_at<LZ, TwoPass<LOGN>::n1 + v>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
     }
   });
 }
 
-template <int LOGN>
+template <int LOGN, bool LZ = false>
 __device__ __forceinline__ void row_fwd_B(u64 (&x)[kEl], const TW* Tr, int c1, u64 q, u64 q2) {
   using P = TwoPass<LOGN>;
   sfor<4, P::n2>([&](auto V_) {
@@ -193,7 +197,7 @@ __device__ __forceinline__ void row_fwd_B(u64 (&x)[kEl], const TW* Tr, int c1, u
     for (int m = 0; m < kEl / (2 * t); ++m) {
       TW w = ldg_tw(Tr + (1 << v) - 1 + m * P::T2 + c1);
 #pragma unroll
-      for (int k = 0; k < t; ++k) ct_bfly(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
+      for (int k = 0; k < t; ++k) ct_bfly_at<LZ, P::n1 + v>(x[m * 2 * t + k], x[m * 2 * t + k + t], w, q, q2);
     }
   });
 }
@@ -264,7 +268,7 @@ __device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
 #else
 #define RNT_ROW_BOUNDS(t) __launch_bounds__(t)
 #endif
-template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC>
+template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC, bool LZ = false>
 __global__ void RNT_ROW_BOUNDS(RPC_ * TwoPass<LOGN>::T2)
 k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
       const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
@@ -300,17 +304,17 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
     row_inv_A<LOGN>(x, Tm, q, q2);
   } else {
     const TW* Tf = tw_row_fwd + troff;
-    row_fwd_A<LOGN>(x, Tf, q, q2);
+    row_fwd_A<LOGN, LZ>(x, Tf, q, q2);
     row_A_to_B<LOGN>(x, rb, c0);
     if (MODE == 2) {
       const u64* bsrc = bop + (b_bcast ? (size_t)l * P::R * P::Cn : u * (size_t)(P::R * P::Cn)) + (size_t)r * P::Cn;
 #pragma unroll
       for (int i = 0; i < kEl; ++i) cp_async8(rb + row_swz<LOGN>(c0 + P::T2 * i), bsrc + c0 + P::T2 * i);
     }
-    row_fwd_B<LOGN>(x, Tf, c0, q, q2);
+    row_fwd_B<LOGN, LZ>(x, Tf, c0, q, q2);
     if (MODE == 0) {
 #pragma unroll
-      for (int i = 0; i < kEl; ++i) x[i] = canon4(x[i], q, q2);
+      for (int i = 0; i < kEl; ++i) x[i] = canon_fwd<LZ>(x[i], q, q2);
       row_B_to_A<LOGN>(x, rb, c0);
     } else {
       cp_async_wait_all();
@@ -400,7 +404,7 @@ k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict
 constexpr int kRowWarps = 2;
 constexpr int kRowKM = 3;
 
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, bool LZ = false>
 __global__ void __launch_bounds__(kRowWarps * 32, 12)
 k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_rows, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
@@ -426,13 +430,14 @@ k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Tm = Tr + (size_t)(P::R - 1 - r0) * N2;     // mirrored row R-1-r0 (- p * N2)
   const TW none{0, 0};
   if constexpr (MODE == 0) {
-    warp_forward<n2, kRowKM, kToGlobal, false, N2>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<n2, kRowKM, kToGlobal, false, N2, LZ, P::n1>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
     warp_inverse<n2, kRowKM, false, false, N2, true>(buf, src, dst, lane, Tm, none, none, q, q2);
   } else {
     const size_t boff = b_bcast ? (size_t)l * P::R * P::Cn : base;
     const GView bview{bop + boff, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
-    warp_polymul<n2, kRowKM, kFromGlobal, false, false, N2, true>(buf, src, dst, bview, nullptr, lane, Tf, Tm, none,
+    warp_polymul<n2, kRowKM, kFromGlobal, false, false, N2, true, LZ, P::n1>(buf, src, dst, bview, nullptr, lane, Tf, Tm,
+                                                                             none,
                                                                   none, q, q2, lc[l].qinv);
   }
 }

@@ -76,7 +76,7 @@ struct PassGeo {
 
 // K CT stages on x[0 .. 2^K) of one group; twiddle w[2^{S+v} + hi 2^v + blk].
 // LZ: lazy ranges for q < 2^60 (ct_bfly_lz; input canonical at stage 0).
-template <int S, int K, bool LZ = false>
+template <int S, int K, bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, u64 q, u64 q2) {
   sfor<0, K>([&](auto V_) {
     constexpr int v = decltype(V_)::value;
@@ -86,10 +86,7 @@ __device__ __forceinline__ void ct_group(u64 (&x)[1 << K], const TW* T, int hi, 
       TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
 #pragma unroll
       for (int k = 0; k < half; ++k) {
-        if constexpr (LZ)
-          ct_bfly_lz<S + v == 7>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
-        else
-          ct_bfly(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+        ct_bfly_at<LZ, S0 + S + v>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
       }
     }
   });
@@ -154,7 +151,8 @@ constexpr int kToBufCanon = 2; // canonical values into the warp buffer
 // ---- one forward pass (CT) over the warp buffer -----------------------------
 // TWS: twiddle-table stride per polynomial of the warp (0: all polynomials
 // share T; 2^{n2}: row r + p of a 2^16 limb uses row table r + p).
-template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false>
+// S0: global index of local stage 0 (rows of a 2^16 limb: n1), for the LZ schedule.
+template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2,
                                          const u64* raw = nullptr) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -177,7 +175,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
-    ct_group<S, K, LZ>(x, T + g.poly * TWS, g.hi, q, q2);
+    ct_group<S, K, LZ, S0>(x, T + g.poly * TWS, g.hi, q, q2);
     if constexpr (DST == kToGlobal) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -235,7 +233,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 // GS pass, all in registers.  b_hat comes from global memory (bview) or from
 // a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf), or a TMA-staged raw buffer (kFromRaw).
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC, bool SCALE = true, int TWS = 0,
-          bool MIRROR = false, bool LZ = false>
+          bool MIRROR = false, bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                           const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv,
                                           const u64* raw = nullptr, const u64* braw = nullptr) {
@@ -273,7 +271,7 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) bv[i] = live ? __ldg(b + i * Geo::LO) : 0ull;
     }
-    ct_group<S, K, LZ>(x, Tf + g.poly * TWS, g.hi, q, q2);
+    ct_group<S, K, LZ, S0>(x, Tf + g.poly * TWS, g.hi, q, q2);
     // a < 16q (LZ, q < 2^60) or < 4q, b_hat < q: a b < q 2^64, result in (0, 2q)
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bv[i], q, qinv);
@@ -302,14 +300,14 @@ struct Passes {
   __host__ __device__ static constexpr int s(int p) { return p * KM; }
 };
 
-template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false>
+template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
     constexpr int SRC = p == 0 ? kFromGlobal : kFromBuf;
     constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ, S0>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
@@ -329,19 +327,19 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
 }
 
 template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false,
-          bool LZ = false>
+          bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using PS = Passes<LOGN, KM>;
   constexpr int NP = PS::NP;
   sfor<0, NP - 1>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS, LZ>(buf, src, dst, lane, Tf, q,
-                                                                                        q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS, LZ, S0>(buf, src, dst, lane, Tf,
+                                                                                            q, q2);
     if constexpr (SYNC) __syncthreads();
   });
   turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR,
-            LZ>(
+            LZ, S0>(
       buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
   if constexpr (SYNC) __syncthreads();
   sfor<0, NP - 1>([&](auto I_) {

@@ -424,7 +424,8 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
                          [{"RNT_CLUSTER_C": "8"}, {"RNT_CLUSTER_C": "16"}, {"RNT_CLUSTER_UNITS": "0"},
                           {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"},
                           {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"},
-                          {"RNT_LAZY": "0", "RNT_LAT_UNITS": "0"}])
+                          {"RNT_LAZY": "0", "RNT_LAT_UNITS": "0"}, {"RNT_LAZY": "0"},
+                          {"RNT_LAZY": "0", "RNT_LARGE_VARIANT": "5"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
@@ -600,19 +601,20 @@ def _primes_below(bits, logn, count):
     return out
 
 
-@pytest.mark.parametrize("logn", [4, 7, 8, 10])
+@pytest.mark.parametrize("logn", [4, 7, 8, 10, 11, 13, 16])
 @pytest.mark.parametrize("bits", [60, 62])
-def test_warp_engine_lazy_ranges(logn, bits):
-    """The batched warp engine (k_warp, > 512 units) at the extremes of its lazy
-    ranges: 60-bit moduli take the LZ kernels (no CT reduction until stage 7,
-    16q bound), moduli in [2^61, 2^62) the Harvey [0, 4q) kernels.  Inputs mix
-    all-(q-1), alternating 0 / q-1, deltas and random residues."""
+def test_lazy_ranges(logn, bits):
+    """The batched engines (k_warp at > 512 units for N <= 2^10, the column/row
+    passes for N >= 2^11) at the extremes of their lazy ranges: 60-bit moduli
+    take the LZ kernels (CT reduction only where the bound would pass 16q:
+    stages 7, 11, 15), moduli in [2^61, 2^62) the Harvey [0, 4q) kernels.
+    Inputs mix all-(q-1), alternating 0 / q-1, deltas and random residues."""
     n = 1 << logn
     ps = _primes_below(bits, logn, 1)
     psi = [O.min_psi(q, logn) for q in ps]
     p = R.Plan(logn, ps)
     q = ps[0]
-    B = 640
+    B = 640 if logn <= 10 else 8
     a = inputs.residues(77 + logn, B, ps, n)
     a[0::4, 0, :] = q - 1
     a[1::8, 0, :] = np.array([0 if i % 2 else q - 1 for i in range(n)], dtype=np.uint64)
