@@ -20,6 +20,7 @@
 #include "ntt_small.cuh"
 #include "keyswitch.cuh"
 #include "ntt_cluster.cuh"
+#include "ntt_clat.cuh"
 #include "plan.h"
 
 using namespace rnt;
@@ -528,9 +529,89 @@ static rnt_status cluster_op_c(const rnt_plan_s* p, int op, u64* out, const u64*
   }
 }
 
+// Latency cluster kernel (ntt_clat.cuh): E coefficients per thread and C CTAs
+// per limb (defaults in clat_op; env RNT_CLAT_E = 4 / 8 and RNT_CLAT_C = 8 / 16
+// override where the geometry is valid); env RNT_CLAT=0 falls back to k_cluster.
+template <int LOGN, int C, int E, int MODE>
+static rnt_status launch_clat_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                                uint32_t batch, cudaStream_t st) {
+  using G = Clat<LOGN, C, E>;
+  auto kern = k_clat<LOGN, C, E, MODE>;
+  static std::atomic<uint64_t> attr{0};
+  if (rnt_status s = ensure_attr(kern, G::SMEM, attr, C > 8); s != RNT_OK) return s;
+  const uint64_t units = (uint64_t)batch * p->L;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * C), 1, 1);
+  cfg.blockDim = dim3(G::TH, 1, 1);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  const TW* cf = p->d_col_fwd;
+  const TW* ci = p->d_col_inv;
+  const TW* rt = p->d_rowtw;
+  const LimbC* lcp = p->d_lc;
+  RNT_CUDA(cudaLaunchKernelEx(&cfg, kern, out, in, bop, bcast, cf, ci, rt, lcp, p->L));
+  return after_launch();
+}
+
+template <int LOGN, int C, int E>
+static constexpr bool clat_valid() {
+  return (1 << LOGN) / C / E >= 32 && (1 << LOGN) / C / E <= 1024 && (1 << (LOGN / 2)) >= C;
+}
+
+template <int LOGN, int C, int E>
+static rnt_status clat_op_ce(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                             uint32_t batch, cudaStream_t st) {
+  switch (op) {
+    case 0: return launch_clat_v<LOGN, C, E, 0>(p, out, in, bop, bcast, batch, st);
+    case 1: return launch_clat_v<LOGN, C, E, 1>(p, out, in, bop, bcast, batch, st);
+    case 2: return launch_clat_v<LOGN, C, E, 2>(p, out, in, bop, bcast, batch, st);
+    default: return RNT_E_INVALID_ARG;
+  }
+}
+
+// Defaults (measured, single-polynomial forward latency under CUDA-graph replay):
+// C = 8 up to 2^12, 16 above; E = 4 (2^12 / 2^13 / 2^14 / 2^15: 3.5 / 3.8 / 5.2 / 8.0 us
+// vs 7.5 / 8.1 / 8.2 / 9.4 us for k_cluster).
+template <int LOGN>
+static rnt_status clat_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                          uint32_t batch, cudaStream_t st) {
+  constexpr int DC = LOGN <= 12 ? 8 : 16, DE = 4;
+  static const int ce = [] {
+    const int c = env_int("RNT_CLAT_C", DC) == 8 ? 8 : 16;
+    const int e = env_int("RNT_CLAT_E", DE) == 8 ? 8 : 4;
+    return c * 16 + e;
+  }();
+  switch (ce) {
+    case 8 * 16 + 4: if constexpr (clat_valid<LOGN, 8, 4>()) return clat_op_ce<LOGN, 8, 4>(p, op, out, in, bop, bcast, batch, st); break;
+    case 8 * 16 + 8: if constexpr (clat_valid<LOGN, 8, 8>()) return clat_op_ce<LOGN, 8, 8>(p, op, out, in, bop, bcast, batch, st); break;
+    case 16 * 16 + 4: if constexpr (clat_valid<LOGN, 16, 4>()) return clat_op_ce<LOGN, 16, 4>(p, op, out, in, bop, bcast, batch, st); break;
+    case 16 * 16 + 8: if constexpr (clat_valid<LOGN, 16, 8>()) return clat_op_ce<LOGN, 16, 8>(p, op, out, in, bop, bcast, batch, st); break;
+    default: break;
+  }
+  static_assert(clat_valid<LOGN, DC, DE>(), "default latency geometry");
+  return clat_op_ce<LOGN, DC, DE>(p, op, out, in, bop, bcast, batch, st);
+}
+
+static bool clat_enabled() {
+  static const bool v = env_int("RNT_CLAT", 1) != 0;
+  return v;
+}
+
 template <int LOGN>
 static rnt_status cluster_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                              uint32_t batch, cudaStream_t st) {
+  // k_clat up to 2^15; at 2^16 the 16-CTA cluster is throughput-bound with 4 coefficients per
+  // thread (13.9 us vs 11.5 us for k_cluster's 16 per thread, CUDA-graph replay)
+  if constexpr (LOGN <= 15) {
+    if (clat_enabled()) return clat_op<LOGN>(p, op, out, in, bop, bcast, batch, st);
+  }
   // cluster size: 8 CTAs up to 2^14, 16 above (measured, single-polynomial
   // latency); env RNT_CLUSTER_C = 8 or 16 forces one
   static const int csz = [] {

@@ -373,8 +373,9 @@ def test_latency_path(logn, limbs, batch, op):
 @pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 1), (1, 2)])
 @pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_bcast"])
 def test_cluster_path(logn, limbs, batch, op):
-    """batch * L <= 2 at N >= 2^11 runs the single-launch cluster kernel
-    (ntt_cluster.cuh: column pass, DSMEM exchange, row pass, exchange, inverse columns)."""
+    """batch * L <= 2 at N >= 2^11 runs a single-launch cluster kernel: k_clat
+    (ntt_clat.cuh, N <= 2^14) or k_cluster (ntt_cluster.cuh): column stages,
+    DSMEM exchange, row stages, exchange, inverse column stages."""
     ps, psi = params(logn, limbs)
     p = R.Plan(logn, ps)
     n = 1 << logn
@@ -402,7 +403,8 @@ sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
 import inputs, oracle as O, paper_2410_05934_b200 as R
 from helpers import params, to_dev, from_dev, empty_dev
 ok = True
-for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3), (16, 9, 1), (12, 8, 1)):
+for logn, limbs, batch in ((10, 1, 37), (10, 2, 5), (16, 3, 2), (13, 2, 3), (16, 9, 1), (12, 8, 1), (11, 2, 1),
+                          (14, 1, 2)):
     ps, psi = params(logn, limbs)
     p = R.Plan(logn, ps)
     a = inputs.residues(3, batch, ps, 1 << logn); b = inputs.residues(4, batch, ps, 1 << logn)
@@ -425,7 +427,9 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
                           {"RNT_CLUSTER_UNITS": "100"}, {"RNT_CLUSTER_UNITS": "100", "RNT_CLUSTER_C": "16"},
                           {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"},
                           {"RNT_LAZY": "0", "RNT_LAT_UNITS": "0"}, {"RNT_LAZY": "0"},
-                          {"RNT_LAZY": "0", "RNT_LARGE_VARIANT": "5"}])
+                          {"RNT_LAZY": "0", "RNT_LARGE_VARIANT": "5"},
+                          {"RNT_CLAT": "0"}, {"RNT_CLAT_E": "8"}, {"RNT_CLAT_C": "16"},
+                          {"RNT_CLAT_C": "16", "RNT_CLAT_E": "8"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
