@@ -538,12 +538,12 @@ static rnt_status launch_clat_v(const rnt_plan_s* p, u64* out, const u64* in, co
   using G = Clat<LOGN, C, E>;
   auto kern = k_clat<LOGN, C, E, MODE>;
   static std::atomic<uint64_t> attr{0};
-  if (rnt_status s = ensure_attr(kern, G::SMEM, attr, C > 8); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(kern, G::template smem<MODE>(), attr, C > 8); s != RNT_OK) return s;
   const uint64_t units = (uint64_t)batch * p->L;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * C), 1, 1);
   cfg.blockDim = dim3(G::TH, 1, 1);
-  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.dynamicSmemBytes = G::template smem<MODE>();
   cfg.stream = st;
   cudaLaunchAttribute a[1];
   a[0].id = cudaLaunchAttributeClusterDimension;

@@ -43,8 +43,19 @@ struct Clat {
   static_assert(CW >= 1 && RC >= 1 && TH >= 32 && TH <= 1024, "cluster latency geometry");
   static constexpr int NP1 = (n1 + KE - 1) / KE;   // column passes
   static constexpr int NP2 = (n2 + KE - 1) / KE;   // row passes
-  static constexpr size_t SMEM = (size_t)(R * CW + RC * RPAD) * 8;
+  static constexpr size_t DATA = (size_t)(R * CW + RC * RPAD) * 8;
+  // + twiddles staged at kernel start: column table(s) [R] and the CTA's row
+  // table(s) [RC][Cn] (forward rows for MODE != 1, mirrored rows for MODE != 0)
+  template <int MODE>
+  static constexpr size_t smem() {
+    return DATA + (size_t)((MODE != 1) + (MODE != 0)) * (R + RC * Cn) * sizeof(TW);
+  }
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 
 // stages covered by pass p of an n-stage phase in radix-2^KE passes
 __host__ __device__ constexpr int clat_k(int n, int KE, int p) { return n - p * KE < KE ? n - p * KE : KE; }
@@ -131,12 +142,36 @@ k_clat(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   auto rpos = [](int j) { return j + (j >> 5); };
   u64 x[E];
 
-  const TW* Tc = tw_col + (size_t)l * R;
-  const TW* Tci = tw_col_inv + (size_t)l * R;
-  const TW* Trows = tw_rows + (size_t)l * R * Cn;
+  // Twiddles this CTA needs, staged into shared memory once with cp.async (one
+  // memory round trip instead of one dependent L2 load per pass): the latency
+  // path is bound by load latency, not by bandwidth.
+  TW* tws = reinterpret_cast<TW*>(sm + G::DATA / 8);
+  TW* sTc = tws;                                       // [R]      forward columns
+  TW* sTr = sTc + (MODE != 1 ? R : 0);                 // [RC][Cn] forward rows k RC + rr
+  TW* sTci = sTr + (MODE != 1 ? RC * Cn : 0);          // [R]      inverse columns
+  TW* sTm = sTci + (MODE != 0 ? R : 0);                // [RC][Cn] mirrored rows R-1-(k RC + rr)
+  {
+    const TW* Trows = tw_rows + (size_t)l * R * Cn;
+    if constexpr (MODE != 1) {
+      for (int i = tid; i < R; i += G::TH) cp_async16(sTc + i, tw_col + (size_t)l * R + i);
+      for (int i = tid; i < RC * Cn; i += G::TH) cp_async16(sTr + i, Trows + (size_t)k * RC * Cn + i);
+    }
+    if constexpr (MODE != 0) {
+      for (int i = tid; i < R; i += G::TH) cp_async16(sTci + i, tw_col_inv + (size_t)l * R + i);
+      for (int i = tid; i < RC * Cn; i += G::TH) {
+        const int rr = i / Cn, e = i % Cn;
+        cp_async16(sTm + i, Trows + (size_t)(R - 1 - (k * RC + rr)) * Cn + e);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  auto tw_ready = [&] {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  };
   // column twiddle of CT/GS stage s at row j: w[2^s + (j >> (n1 - s))]
-  auto twc = [&](int s, int j) { return ldg_tw(Tc + (1 << s) + (j >> (n1 - s))); };
-  auto twci = [&](int s, int j) { return ldg_tw(Tci + (1 << s) + (j >> (n1 - s))); };
+  auto twc = [&](int s, int j) { return sTc[(1 << s) + (j >> (n1 - s))]; };
+  auto twci = [&](int s, int j) { return sTci[(1 << s) + (j >> (n1 - s))]; };
 
   // ---------------- phase A: forward column stages
   if constexpr (MODE != 1) {
@@ -154,6 +189,7 @@ k_clat(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
               p == 0 ? __ldg(in + ubase + (size_t)j * Cn + k * CW + gg[g].line) : tile[j * CW + gg[g].line];
         }
       }
+      if constexpr (p == 0) tw_ready();
 #pragma unroll
       for (int g = 0; g < NG; ++g) clat_ct<S, K, 0>(x + g * (1 << K), gg[g], twc, q, q2);
       if constexpr (p < G::NP1 - 1) {
@@ -186,13 +222,11 @@ k_clat(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
     int rowline = 0;   // set per group (all groups of a thread share the row when NG == 1)
     auto twr = [&](int s, int c) {
       const int v = s - n1;
-      const int r = k * RC + rowline;
-      return ldg_tw(Trows + (size_t)r * Cn + (1 << v) + (c >> (n2 - v)));
+      return sTr[rowline * Cn + (1 << v) + (c >> (n2 - v))];
     };
     auto twrm = [&](int s, int c) {
       const int v = s - n1;
-      const int r = k * RC + rowline;
-      return ldg_tw(Trows + (size_t)(R - 1 - r) * Cn + (2 << v) - 1 - (c >> (n2 - v)));
+      return sTm[rowline * Cn + (2 << v) - 1 - (c >> (n2 - v))];
     };
     if constexpr (MODE != 1) {
       // forward row passes 0 .. NP2-2 (the last one is fused below)
@@ -267,6 +301,7 @@ k_clat(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
                                       ? __ldg(in + ubase + (size_t)(k * RC + gg[g].line) * Cn + gg[g].pos(u))
                                       : recv[gg[g].line * G::RPAD + rpos(gg[g].pos(u))];
         }
+        if constexpr (MODE == 1 && p == G::NP2 - 1) tw_ready();
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
           rowline = gg[g].line;

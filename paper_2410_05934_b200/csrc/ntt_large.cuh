@@ -51,6 +51,12 @@ __device__ __forceinline__ int row_swz(int c) {
 }
 
 // ============================== pass 1 (columns) ==============================
+// (RNT_COL_MINB: experiment knob for the column kernels' min-blocks, like RNT_ROW_MINB.)
+#ifdef RNT_COL_MINB
+#define RNT_COL_BOUNDS(t) __launch_bounds__(t, RNT_COL_MINB)
+#else
+#define RNT_COL_BOUNDS(t) __launch_bounds__(t)
+#endif
 // Forward: CT stages 0..n1-1 on columns [cb*16, cb*16+16) of unit u.
 // MODE 0: plain forward (in -> out).
 // MODUP (key switching, keyswitch.cuh): unit (poly j, limb t) reads limb j of a
@@ -59,7 +65,7 @@ __device__ __forceinline__ int row_swz(int c) {
 // LZ: lazy CT ranges (modarith.cuh ct_bfly_lz, plan flag lazy60); the output
 // then carries the LZ bound of stage n1 and must feed an LZ row pass.
 template <int LOGN, int CT = kColTile, bool MODUP = false, bool LZ = false>
-__global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
+__global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
 k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
@@ -116,7 +122,7 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
 
 // Inverse: GS stages n1-1..0 (+ N^{-1} or N^{-1} R scaling), canonical output.
 template <int LOGN, int CT = kColTile>
-__global__ void __launch_bounds__(CT * TwoPass<LOGN>::T1)
+__global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
 k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
   using P = TwoPass<LOGN>;
