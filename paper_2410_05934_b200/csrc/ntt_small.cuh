@@ -650,6 +650,73 @@ k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restric
   warp_inverse<LOGN, KM>(buf, o1, o1, lane, tw_inv, lc[0].ninvR, lc[0].ninvR_w1, q, q2);
 }
 
+// CTA-parallel external product: one CTA per warp-buffer of slots (1024 / N
+// slots) and one warp per decomposed polynomial r = t l + j (component t,
+// digit j): the 2l forward NTTs run concurrently (k_extprod runs them one after
+// another in a single warp), then all threads form
+// acc_i[e] = sum_r NTT_r[e] (.) z[r][i][e] (Montgomery, [0, 2q)) in warp buffers
+// 0 and 1, and warps 0 / 1 run the two inverse NTTs (N^{-1} 2^64 scale).
+// LV = l (digit levels, 1..8); blockDim = 64 l, dynamic shared memory 2 l warp buffers.
+template <int LOGN, int LV, int KM = 3>
+__global__ void __launch_bounds__(64 * LV)
+k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restrict__ zhat,
+              const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
+              uint32_t n_slot, DigitSpec ds) {
+  using PS = Passes<LOGN, KM>;
+  constexpr int N = 1 << LOGN;
+  constexpr int P = kWarpElems / N;
+  constexpr int NP = PS::NP;
+  static_assert(NP >= 2, "N >= 16");
+  extern __shared__ __align__(16) u64 smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int NW = 2 * LV;        // warps = decomposed polynomials (ds.levels == LV)
+  const uint64_t s0 = (uint64_t)blockIdx.x * P;
+  const u64 q = lc[0].q, q2 = lc[0].q2, qinv = lc[0].qinv;
+  u64* buf = smem + (size_t)warp * kWarpBuf;
+  {
+    const uint32_t t = (uint32_t)warp / LV, j = (uint32_t)warp % LV;
+    const GView cv{c + (uint64_t)t * N, s0, 2ull * N, n_slot};
+    fwd_pass_digit<LOGN, 0, PS::k(0)>(buf, cv, lane, tw_fwd, q, q2, ds, j);
+    sfor<1, NP>([&](auto P_) {
+      constexpr int p = decltype(P_)::value;
+      fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf>(buf, cv, cv, lane, tw_fwd, q, q2);
+    });
+  }
+  __syncthreads();
+  // element e of every warp buffer: slot s0 + e / N, coefficient e % N; each
+  // position is read and rewritten by one thread only
+#pragma unroll 1
+  for (int e = threadIdx.x; e < kWarpElems; e += 32 * NW) {
+    const int k = e & (N - 1);
+    const int pe = wpad(e);
+    u64 z0[NW], z1[NW], x[NW];
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {   // all loads first: one latency for the whole sum
+      z0[r] = __ldg(zhat + (size_t)(2 * r) * N + k);
+      z1[r] = __ldg(zhat + (size_t)(2 * r + 1) * N + k);
+      x[r] = smem[(size_t)r * kWarpBuf + pe];   // lazy [0, 4q)
+    }
+    u64 a0 = 0, a1 = 0;
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      a0 = csub(a0 + mont_mul(x[r], z0[r], q, qinv), q2);
+      a1 = csub(a1 + mont_mul(x[r], z1[r], q, qinv), q2);
+    }
+    smem[pe] = a0;
+    smem[kWarpBuf + pe] = a1;
+  }
+  __syncthreads();
+  if (warp < 2) {
+    const GView o{out + (uint64_t)warp * N, s0, 2ull * N, n_slot};
+    sfor<0, NP>([&](auto I_) {
+      constexpr int p = NP - 1 - decltype(I_)::value;
+      inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(buf, o, o, lane, tw_inv, lc[0].ninvR,
+                                                                   lc[0].ninvR_w1, q, q2);
+    });
+  }
+}
+
 template <int LOGN, int MODE, int W = kTeamWarps>
 inline size_t warp_smem_bytes() {
   return (size_t)W * kWarpBuf * 8 * (MODE == 3 ? 2 : 1);

@@ -489,7 +489,7 @@ def test_automorph_coeff_and_ntt_domain(logn, limbs, batch):
 
 
 @pytest.mark.parametrize("logn,n_slot,bg,l", [(10, 37, 20, 3), (10, 64, 30, 2), (10, 5, 10, 6), (6, 50, 20, 3),
-                                              (4, 70, 15, 4)])
+                                              (4, 70, 15, 4), (10, 9, 8, 8), (8, 13, 31, 1)])
 def test_external_product(logn, n_slot, bg, l):
     """rnt_external_product bit-exact against the oracle, plus the
     gadget-matrix identity c boxtimes G = c."""
@@ -638,3 +638,33 @@ def test_lazy_ranges(logn, bits):
     assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL_EVAL, a, ps, psi, b=bhat, n_threads=8))
     R.polymul(p, d, to_dev(a), to_dev(b), b_is_eval=False)
     assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8))
+
+
+def test_external_product_single_warp_variant():
+    """The single-warp external product kernel (env RNT_EXTPROD=0) stays bit-exact."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {os.path.join(root, 'tests')!r})
+import inputs, oracle as O, paper_2410_05934_b200 as R
+from helpers import params, to_dev, from_dev, empty_dev
+ok = True
+for logn, n_slot, bg, l in ((10, 37, 20, 3), (6, 50, 20, 3)):
+    ps, psi = params(logn, 1)
+    n = 1 << logn
+    p = R.Plan(logn, ps)
+    c = inputs.residues(31, 2 * n_slot, ps, n).reshape(n_slot, 2, n)
+    z = inputs.residues(32, 2 * l * 2, ps, n).reshape(2 * l, 2, n)
+    d = empty_dev(c.shape)
+    R.external_product(p, d, to_dev(c), to_dev(z), bg, l)
+    got = from_dev(d)
+    ok &= all(np.array_equal(got[s], O.external_product(c[s], z, ps[0], psi[0], bg, l)) for s in range(n_slot))
+print("EXT_OK" if ok else "EXT_BAD")
+"""
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RNT_EXTPROD": "0"}, capture_output=True,
+                       text=True, timeout=600)
+    assert "EXT_OK" in r.stdout, r.stdout + r.stderr
