@@ -23,8 +23,9 @@ def host(t):
 
 ok = True
 # (11,2,1), (16,1,1), (12,1,2): cluster kernel; (13,5,1): limb split over streams; (16,2,2): three kernels
+# (13,1,1), (15,1,1): k_clat with 16-CTA clusters; (10,1,520): the LZ warp engine (> 512 units)
 for logn, limbs, batch in ((4, 2, 5), (7, 1, 3), (10, 2, 3), (11, 2, 1), (16, 1, 1), (12, 1, 2), (13, 5, 1),
-                          (16, 2, 2)):
+                          (16, 2, 2), (13, 1, 1), (15, 1, 1), (10, 1, 520)):
     ps = O.primes(logn, limbs)
     psi = [O.min_psi(q, logn) for q in ps]
     p = R.Plan(logn, ps)
@@ -67,5 +68,14 @@ bc = R.BConv(p, pd)
 o2 = torch.empty((2, 2, 1 << 11), dtype=torch.int64, device="cuda")
 bc(o2, dev(a))
 ok &= np.array_equal(host(o2)[0], O.bconv(a[0], ps, O.primes(11, 5)[3:]))
+# external product (CTA-parallel kernel), N = 2^10, l = 3
+ps = O.primes(10, 1)
+p = R.Plan(10, ps)
+c = inputs.residues(7, 2 * 3, ps, 1 << 10).reshape(3, 2, 1 << 10)
+z = inputs.residues(8, 2 * 3 * 2, ps, 1 << 10).reshape(6, 2, 1 << 10)
+o3 = torch.empty(c.shape, dtype=torch.int64, device="cuda")
+R.external_product(p, o3, dev(c), dev(z), 20, 3)
+ok &= all(np.array_equal(host(o3)[s_], O.external_product(c[s_], z, ps[0], O.min_psi(ps[0], 10), 20, 3))
+          for s_ in range(3))
 torch.cuda.synchronize()
 print("sanitize run ok" if ok else "MISMATCH")
