@@ -55,6 +55,7 @@ WORKLOADS = {
 }
 
 L2_FLUSH_BYTES = 256 << 20
+SPIN_CYCLES = 100_000   # ~50 us at 1.965 GHz
 FMA_SLOTS_PER_BFLY = 16   # exact Shoup butterfly: 6 wide/hi multiplies x 2 + 4 IMAD
 IMAD_SLOTS_PER_CLK_SM = 64
 N_SM = 148
@@ -363,6 +364,9 @@ def bench_ours(args, wl, parts):
         barrier()
         for k in range(args.steps):
             flush.zero_()   # L2 flush outside the timed events
+            # device spin outside the events: the step's launches are queued before the
+            # stream reaches the start event, so the events time device execution only
+            torch.cuda._sleep(SPIN_CYCLES)
             step(evs[k], spans[k])
         barrier()
     launches = R.launch_count() - launches0
@@ -448,6 +452,8 @@ def bench_ours(args, wl, parts):
             "data": "synthetic (seeded SplitMix64 uniform residues mod 60-bit NTT primes)",
             "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}",
                        "l2": "flushed (256 MiB write) between steps, outside the timed events",
+                       "launch": "a ~50 us device spin precedes each step's start event (outside the events): "
+                                 "the events time device execution, not host launch latency",
                        "global_polys_per_part": [p[2] * (ws if args.scaling == 'weak' else 1) for p in parts],
                        "parallelism": f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws}, no data-path collective"},
             "gpu_launches": launches,

@@ -346,9 +346,21 @@ static rnt_status lat_dispatch(const rnt_plan_s* p, u64* out, const u64* in, con
   }
 }
 
+static int cluster_units();
+static bool clat_enabled();
+template <int LOGN>
+static rnt_status clat_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
+                          uint32_t batch, cudaStream_t st);
+
 template <int MODE>
 static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                 uint32_t batch, cudaStream_t st) {
+  // single-unit jobs at N = 2^10 (cfg1): the cluster latency kernel spreads the
+  // limb over 8 SMs (k_clat, defined below); polymul with coefficient-form b stays on k_lat
+  if constexpr (MODE <= 2) {
+    if (p->logn == 10 && (uint64_t)batch * p->L <= (uint64_t)cluster_units() && clat_enabled())
+      return clat_op<10>(p, MODE, out, in, bop, bcast, batch, st);
+  }
   if ((uint64_t)batch * p->L <= (uint64_t)lat_units()) return lat_dispatch<MODE>(p, out, in, bop, bcast, batch, st);
   switch (p->logn) {
     case 4: return launch_warp<4, MODE>(p, out, in, bop, bcast, batch, st);
@@ -918,7 +930,10 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   // so only the small column table is kept per direction.
   std::vector<HostTW> nat(n), lay((size_t)n_limbs * n), layi(large ? 0 : (size_t)n_limbs * n);
   std::vector<HostTW> col, coli, rowtw;
-  if (large) {
+  // column / per-row tables: the two-pass kernels (N >= 2^11) and the cluster
+  // latency kernel k_clat (N >= 2^10)
+  const bool ctabs = log2n >= 10;
+  if (ctabs) {
     rowtw.resize((size_t)n_limbs * n);
     col.resize((size_t)n_limbs << n1);
     coli.resize((size_t)n_limbs << n1);
@@ -926,12 +941,12 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   for (uint32_t l = 0; l < n_limbs; ++l) {
     for (int dir = 0; dir < 2; ++dir) {
       plan_powers(limbs[l], log2n, dir == 1, n, nat.data());
-      if (large) {
-        if (dir == 0) {
-          plan_row_layout(nat.data(), log2n, lay.data() + (size_t)l * n);
-          plan_row_natural(nat.data(), log2n, rowtw.data() + (size_t)l * n);
-        }
+      if (ctabs) {
+        if (dir == 0) plan_row_natural(nat.data(), log2n, rowtw.data() + (size_t)l * n);
         std::memcpy((dir ? coli.data() : col.data()) + ((size_t)l << n1), nat.data(), sizeof(HostTW) << n1);
+      }
+      if (large) {
+        if (dir == 0) plan_row_layout(nat.data(), log2n, lay.data() + (size_t)l * n);
       } else {
         HostTW* dst = (dir ? layi.data() : lay.data()) + (size_t)l * n;
         std::memcpy(dst, nat.data(), sizeof(HostTW) * n);  // natural order (ntt_small.cuh)
@@ -951,7 +966,7 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   if ((e = cudaMemcpy(p->d_fwd, lay.data(), sizeof(TW) * lay.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
   if (!large && (e = cudaMemcpy(p->d_inv, layi.data(), sizeof(TW) * layi.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
     return fail(e);
-  if (large) {
+  if (ctabs) {
     if ((e = cudaMalloc(&p->d_col_fwd, sizeof(TW) * col.size())) != cudaSuccess) return fail(e);
     if ((e = cudaMalloc(&p->d_col_inv, sizeof(TW) * coli.size())) != cudaSuccess) return fail(e);
     if ((e = cudaMemcpy(p->d_col_fwd, col.data(), sizeof(TW) * col.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);

@@ -369,12 +369,12 @@ def test_latency_path(logn, limbs, batch, op):
     assert np.array_equal(from_dev(d), want)
 
 
-@pytest.mark.parametrize("logn", [11, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("logn", [10, 11, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 1), (1, 2)])
 @pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_bcast"])
 def test_cluster_path(logn, limbs, batch, op):
-    """batch * L <= 2 at N >= 2^11 runs a single-launch cluster kernel: k_clat
-    (ntt_clat.cuh, N <= 2^14) or k_cluster (ntt_cluster.cuh): column stages,
+    """batch * L <= 2 at N >= 2^10 runs a single-launch cluster kernel: k_clat
+    (ntt_clat.cuh, N <= 2^15) or k_cluster (ntt_cluster.cuh): column stages,
     DSMEM exchange, row stages, exchange, inverse column stages."""
     ps, psi = params(logn, limbs)
     p = R.Plan(logn, ps)
