@@ -802,27 +802,37 @@ static uint32_t ks_split(uint32_t dnum) {
   return (uint32_t)v < dnum ? (uint32_t)v : dnum;
 }
 
-template <int LOGN>
-static rnt_status ks_fused_launch(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk, uint32_t dnum,
-                                  uint32_t split, const KsMod* km, cudaStream_t st) {
+template <int LOGN, bool LZ>
+static rnt_status ks_fused_launch_v(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk,
+                                    uint32_t dnum, uint32_t split, cudaStream_t st) {
   using P = TwoPass<LOGN>;
   const uint32_t LK = qp->L;
   const uint64_t units = (uint64_t)dnum * LK;
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(P::Cn / kColTile, (unsigned)cnt);
-    k_col_fwd<LOGN, kColTile, true><<<g, kColTile * P::T1, 0, st>>>(E, x, qp->d_col_fwd, qp->d_lc, LK, dnum, y0);
+    k_col_fwd<LOGN, kColTile, true, LZ><<<g, kColTile * P::T1, 0, st>>>(E, x, qp->d_col_fwd, qp->d_lc, LK, dnum, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
   constexpr int RPC = P::RPC;
   const size_t smem = (size_t)2 * RPC * P::Cn * 8;
   static std::atomic<uint64_t> attr{0};
-  if (rnt_status s = ensure_attr(k_row_mac<LOGN, RPC>, smem, attr); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(k_row_mac<LOGN, RPC, LZ>, smem, attr); s != RNT_OK) return s;
   dim3 g(P::R / RPC, LK, split);
-  k_row_mac<LOGN, RPC><<<g, RPC * P::T2, smem, st>>>(u, E, evk, qp->d_fwd, qp->d_lc, LK, dnum, split);
-  rnt_status s = after_launch();
+  k_row_mac<LOGN, RPC, LZ><<<g, RPC * P::T2, smem, st>>>(u, E, evk, qp->d_fwd, qp->d_lc, LK, dnum, split);
+  return after_launch();
+}
+
+// lazy CT ranges (LZ) when every prime of Q u P is below 2^60 (the lifted
+// column input is canonical, the Montgomery key product accepts [0, 16q))
+template <int LOGN>
+static rnt_status ks_fused_launch(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk, uint32_t dnum,
+                                  uint32_t split, const KsMod* km, cudaStream_t st) {
+  rnt_status s = (qp->lazy60 && lazy_enabled()) ? ks_fused_launch_v<LOGN, true>(qp, u, E, x, evk, dnum, split, st)
+                                                : ks_fused_launch_v<LOGN, false>(qp, u, E, x, evk, dnum, split, st);
   if (s != RNT_OK || split == 1) return s;
+  const uint32_t LK = qp->L;
   const uint64_t total = 2ull * LK << LOGN;
   uint64_t blocks = (total + 255) / 256;
   const uint64_t cap = (uint64_t)num_sms() * 8;

@@ -346,8 +346,9 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
 // key rows in shared memory, u_k[t] = sum_j NTT(e_j)[t] (.) evk[j][k][t]:
 // the NTT-form extended polynomials never go back to HBM.  Montgomery
 // products, accumulators kept in [0, 2q); u written canonical.
-template <int LOGN, int RPC_>
-__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2)
+// (min-blocks 2: the LZ variant compiled to 130 registers, one CTA per SM)
+template <int LOGN, int RPC_, bool LZ = false>
+__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2, 2)
 k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict__ evk,
           const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t LK, uint32_t dnum,
           uint32_t dsplit) {
@@ -376,9 +377,9 @@ k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict
     u64 x[kEl];
 #pragma unroll
     for (int i = 0; i < kEl; ++i) x[i] = __ldcs(src + P::T2 * i);
-    row_fwd_A<LOGN>(x, Tf, q, q2);
+    row_fwd_A<LOGN, LZ>(x, Tf, q, q2);
     row_A_to_B<LOGN>(x, rb, c0);
-    row_fwd_B<LOGN>(x, Tf, c0, q, q2);
+    row_fwd_B<LOGN, LZ>(x, Tf, c0, q, q2);
     row_B_to_A<LOGN>(x, rb, c0);
     const u64* k0 = evk + ((size_t)(2 * j) * LK + t) * N + roff;
     const u64* k1 = k0 + (size_t)LK * N;
