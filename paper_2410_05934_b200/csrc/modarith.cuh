@@ -110,6 +110,25 @@ __device__ __forceinline__ void ct_bfly_at(u64& X, u64& Y, TW t, u64 q, u64 q2) 
   else ct_bfly(X, Y, t, q, q2);
 }
 
+// GS butterflies of the last three inverse stages without the sum reduction
+// (LZ, q < 2^60): the final stage multiplies both outputs (N^{-1} folded in),
+// and a Shoup product accepts any input below 2^64, so the sum path may grow
+// from [0, 2q) at global stage 2 to [0, 8q) into stage 0 (16q < 2^64).
+// BY = bound of the Y input in units of q (2, 4, 8 at stages 2, 1, 0).
+template <int BY>
+__device__ __forceinline__ void gs_bfly_nr(u64& X, u64& Y, TW t, u64 q, u64 q2) {
+  const u64 d = X + (q2 * (BY / 2)) - Y;   // (0, (BX + BY) q)
+  X = X + Y;                               // [0, (BX + BY) q)
+  Y = shoup_lazy(d, t, q);                 // [0, 2q)
+}
+template <int BY>
+__device__ __forceinline__ void gs_bfly_last_nr(u64& X, u64& Y, TW s0, TW s1, u64 q, u64 q2) {
+  const u64 s = X + Y;
+  const u64 d = X + (q2 * (BY / 2)) - Y;
+  X = shoup_lazy(s, s0, q);
+  Y = shoup_lazy(d, s1, q);
+}
+
 // GS butterfly with a negated twiddle: (X, Y) -> (X + Y, (Y - X) w).  With
 // w = psi^{brv(k')} of the mirrored index k' = 3 2^s - 1 - k this equals the GS
 // butterfly with psi^{-brv(k)} = -psi^{brv(k')}, so inverse row stages can read

@@ -101,14 +101,28 @@ __device__ __forceinline__ u64 canon_fwd(u64 x, u64 q, u64 q2) {
 
 // K GS stages (reverse order).  If LAST (S == 0), local stage 0 is the final
 // stage of the inverse and carries the N^{-1} (or N^{-1} R) factor.
-template <int S, int K, bool LAST, bool MIRROR = false>
+// LZT: the inverse ends with the scaled stage 0 and q < 2^60: global stages
+// 2, 1, 0 skip the sum reduction (gs_bfly_nr / gs_bfly_last_nr).
+template <int S, int K, bool LAST, bool MIRROR = false, bool LZT = false>
 __device__ __forceinline__ void gs_group(u64 (&x)[1 << K], const TW* T, int hi, TW s0, TW s1, u64 q, u64 q2) {
+  static_assert(!(LZT && MIRROR), "LZ tail needs the scaled last stage");
   sfor<0, K>([&](auto I_) {
     constexpr int v = K - 1 - decltype(I_)::value;
     constexpr int half = (1 << K) >> (v + 1);
     if constexpr (LAST && v == 0) {
 #pragma unroll
-      for (int k = 0; k < half; ++k) gs_bfly_last(x[k], x[k + half], s0, s1, q, q2);
+      for (int k = 0; k < half; ++k) {
+        if constexpr (LZT && S == 0) gs_bfly_last_nr<8>(x[k], x[k + half], s0, s1, q, q2);
+        else gs_bfly_last(x[k], x[k + half], s0, s1, q, q2);
+      }
+    } else if constexpr (LZT && S + v <= 2) {
+#pragma unroll
+      for (int blk = 0; blk < (1 << v); ++blk) {
+        TW w = ldg_tw(T + (1 << (S + v)) + hi * (1 << v) + blk);
+#pragma unroll
+        for (int k = 0; k < half; ++k)
+          gs_bfly_nr<(2 << (2 - (S + v)))>(x[blk * 2 * half + k], x[blk * 2 * half + k + half], w, q, q2);
+      }
     } else {
 #pragma unroll
       for (int blk = 0; blk < (1 << v); ++blk) {
@@ -191,7 +205,8 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
   __syncwarp();
 }
 
-template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST, int TWS = 0, bool MIRROR = false>
+template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST, int TWS = 0, bool MIRROR = false,
+          bool LZT = false>
 __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                          u64 q, u64 q2, const u64* raw = nullptr) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -214,7 +229,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
     }
-    gs_group<S, K, LAST, MIRROR>(x, MIRROR ? T - g.poly * TWS : T + g.poly * TWS, g.hi, s0, s1, q, q2);
+    gs_group<S, K, LAST, MIRROR, LZT>(x, MIRROR ? T - g.poly * TWS : T + g.poly * TWS, g.hi, s0, s1, q, q2);
     if constexpr (DST_GLOBAL) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -275,7 +290,8 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
     // a < 16q (LZ, q < 2^60) or < 4q, b_hat < q: a b < q 2^64, result in (0, 2q)
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = mont_mul(x[i], bv[i], q, qinv);
-    gs_group<S, K, SCALE && S == 0, MIRROR>(x, MIRROR ? Ti - g.poly * TWS : Ti + g.poly * TWS, g.hi, s0, s1, q, q2);
+    gs_group<S, K, SCALE && S == 0, MIRROR, LZ && SCALE>(x, MIRROR ? Ti - g.poly * TWS : Ti + g.poly * TWS, g.hi, s0,
+                                                         s1, q, q2);
     if constexpr (DST_GLOBAL) {
       if (dst.live(g.poly)) {
         u64* d = const_cast<u64*>(dst.at(g.poly)) + jj0;
@@ -312,7 +328,7 @@ __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int
   });
 }
 
-template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false>
+template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false, bool LZ = false>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
@@ -320,8 +336,8 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
     constexpr int i = decltype(I_)::value;
     constexpr int p = PS::NP - 1 - i;
     constexpr int SRC = i == 0 ? kFromGlobal : kFromBuf;
-    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR>(buf, src, dst, lane, T, s0, s1, q,
-                                                                                  q2);
+    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE>(buf, src, dst, lane,
+                                                                                                T, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
@@ -344,7 +360,8 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
   if constexpr (SYNC) __syncthreads();
   sfor<0, NP - 1>([&](auto I_) {
     constexpr int p = NP - 2 - decltype(I_)::value;
-    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, SCALE && p == 0, TWS, MIRROR>(buf, src, dst, lane, Ti, s0, s1,
+    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE>(buf, src, dst,
+                                                                                                     lane, Ti, s0, s1,
                                                                                        q, q2);
     if constexpr (SYNC) __syncthreads();
   });
@@ -379,7 +396,7 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   if constexpr (MODE == 0) {
     warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<LOGN, KM, SYNC>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+    warp_inverse<LOGN, KM, SYNC, true, 0, false, LZ>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
   } else {
     const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
     const u64 qinv = lc[l].qinv;
