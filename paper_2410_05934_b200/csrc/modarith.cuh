@@ -65,7 +65,14 @@ __device__ __forceinline__ u64 shoup_lazy(u64 y, TW t, u64 q) {
   return y * t.w - Q * q;
 }
 
-__device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+// x - m if x >= m else x, for x < 2m and m < 2^63 (every call site: lazy
+// bounds 2m at most): the sign of the 64-bit difference decides, one compare
+// instead of the unsigned compare pair (ptxas then drops an IMAD.IADD from
+// the fmaheavy pipe per butterfly).
+__device__ __forceinline__ u64 csub(u64 x, u64 m) {
+  const u64 d = x - m;
+  return (long long)d < 0 ? x : d;
+}
 
 __device__ __forceinline__ void ct_bfly(u64& X, u64& Y, TW t, u64 q, u64 q2) {
   u64 x = csub(X, q2);          // [0, 2q)
