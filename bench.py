@@ -313,13 +313,18 @@ def bench_ours(args, wl, parts):
     dom = int(np.argmax(work)) if work else 0
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
-    run_streams = [torch.cuda.Stream() for _ in states] if args.concurrent_parts else [stream for _ in states]
+    # independent parts (cfg5: the 2^16 x 45 polynomial and the 2^10 batch) run on
+    # their own streams so each fills the other's ramp and tail (--sequential-parts: one stream)
+    concurrent = args.concurrent_parts and len(states) > 1
+    run_streams = [torch.cuda.Stream() for _ in states] if concurrent else [stream for _ in states]
+    seq_streams = [stream for _ in states]
 
-    def step(ev=None, span=None):
+    def step(ev=None, span=None, streams=None):
+        streams = run_streams if streams is None else streams
         if span is not None:
             span[0].record(stream)
         for i, s in enumerate(states):
-            rs = run_streams[i]
+            rs = streams[i]
             if rs is not stream:
                 rs.wait_stream(stream)
             if ev is not None:
@@ -327,7 +332,7 @@ def bench_ours(args, wl, parts):
             R.polymul(s["plan"], s["c"], s["a"], s["b"], b_is_eval=True, stream=rs)
             if ev is not None:
                 ev[i][1].record(rs)
-        for rs in run_streams:
+        for rs in streams:
             if rs is not stream:
                 stream.wait_stream(rs)
         if span is not None:
@@ -374,6 +379,21 @@ def bench_ours(args, wl, parts):
     step_ms = [spans[k][0].elapsed_time(spans[k][1]) for k in range(args.steps)]
     total_ms = sum(step_ms)
 
+    # ---- per-kernel times for the roofline: with concurrent parts the timed
+    # region overlaps them, so each part is also timed alone (one stream, L2
+    # flushed, same spin) in a short sequential pass
+    part_ms_seq = part_ms
+    if concurrent:
+        nseq = min(args.steps, 20)
+        sevs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in states] for _ in range(nseq)]
+        barrier()
+        for k in range(nseq):
+            flush.zero_()
+            torch.cuda._sleep(SPIN_CYCLES)
+            step(sevs[k], None, seq_streams)
+        barrier()
+        part_ms_seq = [[sevs[k][i][0].elapsed_time(sevs[k][i][1]) for k in range(nseq)] for i in range(len(states))]
+
     # ---- secondary: L2-warm (no flush between steps; inputs partly L2-resident)
     warm_spans = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(min(args.steps, 50))]
     barrier()
@@ -416,7 +436,7 @@ def bench_ours(args, wl, parts):
     peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9   # Gbfly/s
     s = states[dom]
     bfly_launch = 2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]
-    dom_ms = statistics.mean(part_ms[dom])
+    dom_ms = statistics.mean(part_ms_seq[dom])
     achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -433,7 +453,7 @@ def bench_ours(args, wl, parts):
                           f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
     parts_out = []
     for i, st in enumerate(states):
-        ms = statistics.mean(part_ms[i])
+        ms = statistics.mean(part_ms_seq[i])
         xf = 2 * st["limbs"] * st["polys"]
         bf = xf * (1 << st["logn"]) // 2 * st["logn"]
         alg_bytes = 3 * st["limbs"] * st["polys"] * (1 << st["logn"]) * 8  # read a, b_hat; write c
@@ -463,6 +483,9 @@ def bench_ours(args, wl, parts):
                         "note": "secondary: no L2 flush between steps, rank 0"},
             "roofline": roof,
             "parts": parts_out,
+            "parts_schedule": ("concurrent: the parts run on separate streams inside each timed step; roofline "
+                               "and parts[].ms come from a sequential pass after the timed region (each part "
+                               "alone, L2 flushed)") if concurrent else "sequential: one stream",
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
             "clocks": clk.summary(),
         }
@@ -772,7 +795,9 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
-    ap.add_argument("--concurrent-parts", action="store_true",
+    ap.add_argument("--sequential-parts", dest="concurrent_parts", action="store_false",
+                    help="run the parts of a step one after another on one stream (default: concurrent)")
+    ap.add_argument("--concurrent-parts", dest="concurrent_parts", action="store_true",
                     help="run the independent parts of a step on separate streams")
     ap.add_argument("--latency", action="store_true", help="paper-comparable single-polynomial latency mode")
     ap.add_argument("--automorph", action="store_true", help="SURVEY f4 automorph bandwidth mode")
