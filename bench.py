@@ -447,8 +447,13 @@ def bench_ours(args, wl, parts):
             traffic = None
     kern = f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch)" if s["logn"] <= 10 else \
         f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
+    # whole step: every butterfly of every part over the timed step time (all ranks)
+    step_bfly = sum(2 * st["limbs"] * st["polys"] * (1 << st["logn"]) // 2 * st["logn"] for st in states) * (
+        ws if args.scaling == "weak" else 1)
+    step_achieved = step_bfly * args.steps / (total_ms * 1e-3) / 1e9 / ws
     roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak_bfly,
             "unit": "Gbutterfly/s", "frac": achieved / peak_bfly, "traffic": traffic,
+            "step_achieved_per_gpu": step_achieved, "step_frac": step_achieved / peak_bfly,
             "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
                           f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
     parts_out = []
