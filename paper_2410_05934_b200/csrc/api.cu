@@ -227,18 +227,18 @@ static rnt_status set_smem(K kern, size_t smem) {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false>
+template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false, bool PF = false>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
-  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ>, smem, attr); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ, PF>, smem, attr); s != RNT_OK) return s;
   const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ><<<grid, W * 32, smem, st>>>(
+    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ, PF><<<grid, W * 32, smem, st>>>(
         out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
         p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
@@ -251,6 +251,15 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
 // configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
 static int small_variant() {
   static const int v = env_int("RNT_SMALL_VARIANT", 0);
+  return v;
+}
+
+// env RNT_PREFETCH=1: stage each warp's polynomials with cp.async before the
+// first pass (k_warp PF).  Off by default: measured slower (cfg5 k_warp 0.2676 vs
+// 0.2647 ms) -- six warps per SMSP already hide the per-group loads, and the
+// staging puts every load of the warp ahead of any arithmetic.
+static bool prefetch_enabled() {
+  static const bool v = env_int("RNT_PREFETCH", 0) != 0;
   return v;
 }
 
@@ -309,7 +318,10 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   // default: radix-8 passes (N=2^10: 3+3+3+1), 2 warps per CTA, <= 85 registers
   // (24 warps/SM) -- fastest measured (profiles/r01/README.md); lazy CT ranges
   // when every modulus is below 2^60 (env RNT_LAZY=0 disables)
-  if (p->lazy60 && lazy_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
+  if (p->lazy60 && lazy_enabled()) {
+    if (prefetch_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true, true>(p, out, in, bop, bcast, batch, st);
+    return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
+  }
   return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 

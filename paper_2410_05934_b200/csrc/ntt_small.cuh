@@ -316,26 +316,29 @@ struct Passes {
   __host__ __device__ static constexpr int s(int p) { return p * KM; }
 };
 
-template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0>
+// SRC0: source of the first pass (kFromGlobal, or kFromBuf after warp_prefetch).
+template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0,
+          int SRC0 = kFromGlobal>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    constexpr int SRC = p == 0 ? kFromGlobal : kFromBuf;
+    constexpr int SRC = p == 0 ? SRC0 : kFromBuf;
     constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
     fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ, S0>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
 
-template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false, bool LZ = false>
+template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false, bool LZ = false,
+          int SRC0 = kFromGlobal>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto I_) {
     constexpr int i = decltype(I_)::value;
     constexpr int p = PS::NP - 1 - i;
-    constexpr int SRC = i == 0 ? kFromGlobal : kFromBuf;
+    constexpr int SRC = i == 0 ? SRC0 : kFromBuf;
     inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE>(buf, src, dst, lane,
                                                                                                 T, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
@@ -343,18 +346,18 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
 }
 
 template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false,
-          bool LZ = false, int S0 = 0>
+          bool LZ = false, int S0 = 0, int SRC0 = kFromGlobal>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using PS = Passes<LOGN, KM>;
   constexpr int NP = PS::NP;
   sfor<0, NP - 1>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? kFromGlobal : kFromBuf, kToBuf, TWS, LZ, S0>(buf, src, dst, lane, Tf,
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? SRC0 : kFromBuf, kToBuf, TWS, LZ, S0>(buf, src, dst, lane, Tf,
                                                                                             q, q2);
     if constexpr (SYNC) __syncthreads();
   });
-  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? kFromGlobal : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR,
+  turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? SRC0 : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR,
             LZ, S0>(
       buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
   if constexpr (SYNC) __syncthreads();
@@ -372,8 +375,25 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
+// Stage the warp's polynomials into its (padded) buffer with 8-byte cp.async:
+// every global load of the first pass is in flight at once instead of one
+// group's loads per loop iteration (PF kernels).
+template <int LOGN>
+__device__ __forceinline__ void warp_prefetch(u64* buf, const GView& src, int lane) {
+  constexpr int N = 1 << LOGN;
+#pragma unroll 4
+  for (int j = lane; j < kWarpElems; j += 32) {
+    const int poly = j >> LOGN;
+    if (src.live(poly)) cp_async8(buf + wpad(j), src.at(poly) + (j & (N - 1)));
+  }
+  cp_async_wait_all();
+  __syncwarp();
+}
+
 // LZ: lazy CT ranges (ct_bfly_lz), valid when every modulus of the plan is < 2^60.
-template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false>
+// PF: first pass from shared memory after warp_prefetch (MODE 0, 1, 2).
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false,
+          bool PF = false>
 __global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
@@ -393,10 +413,14 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const GView dst{out + (uint64_t)l * N, p0, stride, B};
   const TW* Tf = tw_fwd + (size_t)l * N;
   const TW* Ti = tw_inv + (size_t)l * N;
+  constexpr bool PFM = PF && MODE != 3;
+  constexpr int SRC0 = PFM ? kFromBuf : kFromGlobal;
+  if constexpr (PFM) warp_prefetch<LOGN>(buf, src, lane);
   if constexpr (MODE == 0) {
-    warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ, 0, SRC0>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<LOGN, KM, SYNC, true, 0, false, LZ>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
+    warp_inverse<LOGN, KM, SYNC, true, 0, false, LZ, SRC0>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q,
+                                                           q2);
   } else {
     const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
     const u64 qinv = lc[l].qinv;
@@ -406,8 +430,8 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
       warp_forward<LOGN, KM, kToBufCanon, SYNC, 0, LZ>(bbuf, bview, bview, lane, Tf, q, q2);
       warp_polymul<LOGN, KM, kFromBuf, SYNC, true, 0, false, LZ>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     } else {
-      warp_polymul<LOGN, KM, kFromGlobal, SYNC, true, 0, false, LZ>(buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2,
-                                qinv);
+      warp_polymul<LOGN, KM, kFromGlobal, SYNC, true, 0, false, LZ, 0, SRC0>(buf, src, dst, bview, nullptr, lane, Tf,
+                                                                         Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     }
   }
 }
