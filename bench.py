@@ -304,8 +304,9 @@ def bench_ours(args, wl, parts):
         db = torch.from_numpy(bhat.view(np.int64)).to(dev)
         dc = torch.empty_like(da)
         ha = torch.from_numpy(a.view(np.int64)).pin_memory()
-        hc = torch.empty_like(ha).pin_memory()
-        ws_buf = torch.empty_like(da)
+        # two output / workspace sets: consecutive e2e steps alternate between them
+        hc = [torch.empty_like(ha).pin_memory() for _ in range(2)]
+        ws_buf = [torch.empty_like(da) for _ in range(2)]
         states.append(dict(logn=logn, limbs=len(mods), polys=polys, plan=plan, a=da, b=db, c=dc,
                            ha=ha, hc=hc, ws=ws_buf))
     # the dominant kernel: largest butterfly count part
@@ -339,17 +340,29 @@ def bench_ours(args, wl, parts):
             span[1].record(stream)
 
     # end to end: each part on its own user stream (independent batches overlap
-    # their PCIe traffic); the library pipelines chunks inside each call.
-    part_streams = [torch.cuda.Stream() for _ in states]
+    # their PCIe traffic); the library pipelines chunks inside each call.  Step k
+    # uses buffer set / stream set k % 2, so step k+1's host->device copies queue
+    # right behind step k's on the library's copy stream (streaming) while set k % 2
+    # is reused only after step k - 2 completed (same user stream).
+    part_streams = [[torch.cuda.Stream() for _ in states] for _ in range(2)]
 
-    def step_host():
+    def step_host(k=0):
+        sset = k % 2 if args.e2e_overlap else 0
+        for s, ps in zip(states, part_streams[sset]):
+            R.execute_host(s["plan"], R.OP_POLYMUL_EVAL, s["hc"][sset], s["ha"], s["ws"][sset], b_dev=s["b"],
+                           stream=ps)
+
+    def e2e_fork():
         ev = torch.cuda.Event()
         ev.record(stream)
-        for s, ps in zip(states, part_streams):
-            ps.wait_event(ev)
-            R.execute_host(s["plan"], R.OP_POLYMUL_EVAL, s["hc"], s["ha"], s["ws"], b_dev=s["b"], stream=ps)
-        for ps in part_streams:
-            stream.wait_stream(ps)
+        for pss in part_streams:
+            for ps in pss:
+                ps.wait_event(ev)
+
+    def e2e_join():
+        for pss in part_streams:
+            for ps in pss:
+                stream.wait_stream(ps)
 
     def barrier():
         torch.cuda.synchronize()
@@ -405,14 +418,21 @@ def bench_ours(args, wl, parts):
     # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
     e2e_ms = float("nan")
     if args.e2e:
-        for _ in range(max(1, args.warmup // 2)):
-            step_host()
+        e2e_fork()
+        for k in range(max(2, args.warmup // 2)):
+            step_host(k)
+        e2e_join()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
+        e2e_fork()
         for k in range(args.steps):
-            step_host()
+            if not args.e2e_overlap:
+                e2e_join()
+                e2e_fork()
+            step_host(k)
+        e2e_join()
         e1.record(stream)
         barrier()
         e2e_ms = e0.elapsed_time(e1)
@@ -491,7 +511,9 @@ def bench_ours(args, wl, parts):
             "parts_schedule": ("concurrent: the parts run on separate streams inside each timed step; roofline "
                                "and parts[].ms come from a sequential pass after the timed region (each part "
                                "alone, L2 flushed)") if concurrent else "sequential: one stream",
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d,
+                    "schedule": ("streamed: consecutive steps alternate two buffer sets, step k+1's copies queue "
+                                 "behind step k's") if args.e2e_overlap else "serial: each step joins before the next"},
             "clocks": clk.summary(),
         }
         if args.cpu_baseline and ws >= 1 and rank == 0 and (ws == 1):
@@ -800,6 +822,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
+    ap.add_argument("--e2e-serial", dest="e2e_overlap", action="store_false",
+                    help="e2e: join every step before the next (default: consecutive steps stream)")
     ap.add_argument("--sequential-parts", dest="concurrent_parts", action="store_false",
                     help="run the parts of a step one after another on one stream (default: concurrent)")
     ap.add_argument("--concurrent-parts", dest="concurrent_parts", action="store_true",
