@@ -312,15 +312,20 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
       case 12: return launch_warp_v<LOGN, MODE, 4, 6, false, 3>(p, out, in, bop, bcast, batch, st);
       case 13: return launch_warp_v<LOGN, MODE, 2, 16, false, 2>(p, out, in, bop, bcast, batch, st);
       case 14: return launch_warp_v<LOGN, MODE, 1, 24, false, 3>(p, out, in, bop, bcast, batch, st);
+      case 16:   // LZ with the plain radix-8 schedule 3 + 3 + 3 + 1 (the default before the split tail)
+        if (p->lazy60) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
+        break;
       default: break;
     }
   }
   // default: radix-8 passes (N=2^10: 3+3+3+1), 2 warps per CTA, <= 85 registers
   // (24 warps/SM) -- fastest measured (profiles/r01/README.md); lazy CT ranges
   // when every modulus is below 2^60 (env RNT_LAZY=0 disables)
+  // LZ kernels use the split-tail schedule (N = 2^10: 3 + 3 + 2 + 2; cfg5 k_warp 0.2643 -> 0.2623
+  // ms, cfg2 0.0847 -> 0.0813 ms): the polymul turn pass works on 4-coefficient groups
   if (p->lazy60 && lazy_enabled()) {
-    if (prefetch_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true, true>(p, out, in, bop, bcast, batch, st);
-    return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
+    if (prefetch_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true, true>(p, out, in, bop, bcast, batch, st);
+    return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true>(p, out, in, bop, bcast, batch, st);
   }
   return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }

@@ -311,10 +311,20 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
 // remainder), e.g. N = 2^10: KM = 4 -> 4 + 4 + 2, KM = 3 -> 3 + 3 + 3 + 1.
 template <int LOGN, int KM>
 struct Passes {
-  static constexpr int NP = (LOGN + KM - 1) / KM;
-  __host__ __device__ static constexpr int k(int p) { return p < NP - 1 ? KM : LOGN - KM * (NP - 1); }
-  __host__ __device__ static constexpr int s(int p) { return p * KM; }
+  // KM >= 10 encodes radix KM / 10 with a split tail: when LOGN leaves a
+  // remainder of 1, the last two passes take (B - 1, 2) stages instead of (B, 1)
+  // (N = 2^10, KM = 32: 3 + 3 + 2 + 2), so the fused polymul turn pass holds
+  // 4-coefficient groups.
+  static constexpr int B = KM >= 10 ? KM / 10 : KM;
+  static constexpr int NP = (LOGN + B - 1) / B;
+  static constexpr bool SPLIT = KM >= 10 && NP >= 2 && LOGN - B * (NP - 1) == 1 && B >= 3;
+  __host__ __device__ static constexpr int k(int p) {
+    return SPLIT ? (p < NP - 2 ? B : (p == NP - 2 ? B - 1 : 2)) : (p < NP - 1 ? B : LOGN - B * (NP - 1));
+  }
+  __host__ __device__ static constexpr int s(int p) { return (SPLIT && p == NP - 1) ? B * (NP - 2) + B - 1 : p * B; }
 };
+static_assert(Passes<10, 32>::k(2) == 2 && Passes<10, 32>::k(3) == 2 && Passes<10, 32>::s(3) == 8, "split tail");
+static_assert(Passes<10, 3>::k(3) == 1 && Passes<10, 3>::s(3) == 9, "radix-8 schedule");
 
 // SRC0: source of the first pass (kFromGlobal, or kFromBuf after warp_prefetch).
 template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0,

@@ -420,7 +420,7 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
 """
 
 
-@pytest.mark.parametrize("env", [{"RNT_SMALL_VARIANT": str(v)} for v in (1, 4, 5, 6, 7, 8, 11, 13)] +
+@pytest.mark.parametrize("env", [{"RNT_SMALL_VARIANT": str(v)} for v in (1, 4, 5, 6, 7, 8, 11, 13, 16)] +
                          [{"RNT_LARGE_VARIANT": str(v)} for v in (1, 2, 4, 5)] +
                          [{"RNT_SPLIT": str(v)} for v in (0, 3, 4)] +
                          [{"RNT_CLUSTER_C": "8"}, {"RNT_CLUSTER_C": "16"}, {"RNT_CLUSTER_UNITS": "0"},
