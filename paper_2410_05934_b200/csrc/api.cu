@@ -739,16 +739,25 @@ struct rnt_bconv_s {
 // (N = 2^10, l = 3: 1024 / 4096 / 16384 slots 0.127 / 0.411 / 1.55 ms vs 0.209 /
 // 0.537 / 1.73 ms for the single-warp k_extprod); env RNT_EXTPROD=0 selects k_extprod.
 
+template <int LOGN, int LV, int KM, bool LZ>
+static rnt_status launch_extprod_cta_v(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
+                                       DigitSpec ds, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  const size_t smem = (size_t)2 * LV * kWarpBuf * 8;
+  if (rnt_status s = ensure_attr(k_extprod_cta<LOGN, LV, KM, LZ>, smem, attr); s != RNT_OK) return s;
+  const uint64_t per_cta = kWarpElems >> LOGN;
+  const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
+  k_extprod_cta<LOGN, LV, KM, LZ><<<(unsigned)grid, 64 * LV, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc,
+                                                                          n_slot, ds);
+  return after_launch();
+}
+
+// LZ kernels (split-tail schedule) when the modulus is below 2^60
 template <int LOGN, int LV>
 static rnt_status launch_extprod_cta(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                      DigitSpec ds, cudaStream_t st) {
-  static std::atomic<uint64_t> attr{0};
-  const size_t smem = (size_t)2 * LV * kWarpBuf * 8;
-  if (rnt_status s = ensure_attr(k_extprod_cta<LOGN, LV>, smem, attr); s != RNT_OK) return s;
-  const uint64_t per_cta = kWarpElems >> LOGN;
-  const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
-  k_extprod_cta<LOGN, LV><<<(unsigned)grid, 64 * LV, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc, n_slot, ds);
-  return after_launch();
+  if (p->lazy60 && lazy_enabled()) return launch_extprod_cta_v<LOGN, LV, 32, true>(p, out, c, z, n_slot, ds, st);
+  return launch_extprod_cta_v<LOGN, LV, 3, false>(p, out, c, z, n_slot, ds, st);
 }
 
 template <int LOGN>

@@ -609,7 +609,7 @@ __device__ __forceinline__ u64 gadget_digit(u64 v, u64 q, const DigitSpec& ds, u
 }
 
 // first forward pass of digit j of component view `src`
-template <int LOGN, int S, int K>
+template <int LOGN, int S, int K, bool LZ = false>
 __device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, const TW* T, u64 q, u64 q2,
                                                const DigitSpec& ds, uint32_t j) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -624,7 +624,7 @@ __device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, co
     u64 x[1 << K];
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) x[i] = live ? gadget_digit(sp[i * Geo::LO], q, ds, j) : 0ull;
-    ct_group<S, K>(x, T, g.hi, q, q2);
+    ct_group<S, K, LZ>(x, T, g.hi, q, q2);
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
   }
@@ -708,7 +708,8 @@ k_extprod(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restric
 // acc_i[e] = sum_r NTT_r[e] (.) z[r][i][e] (Montgomery, [0, 2q)) in warp buffers
 // 0 and 1, and warps 0 / 1 run the two inverse NTTs (N^{-1} 2^64 scale).
 // LV = l (digit levels, 1..8); blockDim = 64 l, dynamic shared memory 2 l warp buffers.
-template <int LOGN, int LV, int KM = 3>
+// LZ: lazy CT ranges / inverse tail (q < 2^60; the digits are canonical residues).
+template <int LOGN, int LV, int KM = 3, bool LZ = false>
 __global__ void __launch_bounds__(64 * LV)
 k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __restrict__ zhat,
               const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
@@ -728,10 +729,10 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
   {
     const uint32_t t = (uint32_t)warp / LV, j = (uint32_t)warp % LV;
     const GView cv{c + (uint64_t)t * N, s0, 2ull * N, n_slot};
-    fwd_pass_digit<LOGN, 0, PS::k(0)>(buf, cv, lane, tw_fwd, q, q2, ds, j);
+    fwd_pass_digit<LOGN, 0, PS::k(0), LZ>(buf, cv, lane, tw_fwd, q, q2, ds, j);
     sfor<1, NP>([&](auto P_) {
       constexpr int p = decltype(P_)::value;
-      fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf>(buf, cv, cv, lane, tw_fwd, q, q2);
+      fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf, 0, LZ>(buf, cv, cv, lane, tw_fwd, q, q2);
     });
   }
   __syncthreads();
@@ -762,8 +763,8 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
     const GView o{out + (uint64_t)warp * N, s0, 2ull * N, n_slot};
     sfor<0, NP>([&](auto I_) {
       constexpr int p = NP - 1 - decltype(I_)::value;
-      inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0>(buf, o, o, lane, tw_inv, lc[0].ninvR,
-                                                                   lc[0].ninvR_w1, q, q2);
+      inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0, 0, false, LZ>(buf, o, o, lane, tw_inv,
+                                                                                 lc[0].ninvR, lc[0].ninvR_w1, q, q2);
     });
   }
 }

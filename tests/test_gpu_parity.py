@@ -641,8 +641,10 @@ def test_lazy_ranges(logn, bits):
     assert np.array_equal(from_dev(d), O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8))
 
 
-def test_external_product_single_warp_variant():
-    """The single-warp external product kernel (env RNT_EXTPROD=0) stays bit-exact."""
+@pytest.mark.parametrize("env", [{"RNT_EXTPROD": "0"}, {"RNT_LAZY": "0"}])
+def test_external_product_single_warp_variant(env):
+    """The single-warp external product kernel (env RNT_EXTPROD=0) and the CTA kernel
+    without lazy ranges (RNT_LAZY=0) stay bit-exact."""
     import os
     import subprocess
     import sys
@@ -666,6 +668,6 @@ for logn, n_slot, bg, l in ((10, 37, 20, 3), (6, 50, 20, 3)):
     ok &= all(np.array_equal(got[s], O.external_product(c[s], z, ps[0], psi[0], bg, l)) for s in range(n_slot))
 print("EXT_OK" if ok else "EXT_BAD")
 """
-    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "RNT_EXTPROD": "0"}, capture_output=True,
-                       text=True, timeout=600)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
     assert "EXT_OK" in r.stdout, r.stdout + r.stderr
