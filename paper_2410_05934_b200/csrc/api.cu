@@ -227,18 +227,18 @@ static rnt_status set_smem(K kern, size_t smem) {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false, bool PF = false>
+template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
-  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ, PF>, smem, attr); s != RNT_OK) return s;
+  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ>, smem, attr); s != RNT_OK) return s;
   const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ, PF><<<grid, W * 32, smem, st>>>(
+    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ><<<grid, W * 32, smem, st>>>(
         out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
         p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
@@ -251,15 +251,6 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
 // configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
 static int small_variant() {
   static const int v = env_int("RNT_SMALL_VARIANT", 0);
-  return v;
-}
-
-// env RNT_PREFETCH=1: stage each warp's polynomials with cp.async before the
-// first pass (k_warp PF).  Off by default: measured slower (cfg5 k_warp 0.2676 vs
-// 0.2647 ms) -- six warps per SMSP already hide the per-group loads, and the
-// staging puts every load of the warp ahead of any arithmetic.
-static bool prefetch_enabled() {
-  static const bool v = env_int("RNT_PREFETCH", 0) != 0;
   return v;
 }
 
@@ -323,10 +314,7 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   // when every modulus is below 2^60 (env RNT_LAZY=0 disables)
   // LZ kernels use the split-tail schedule (N = 2^10: 3 + 3 + 2 + 2; cfg5 k_warp 0.2643 -> 0.2623
   // ms, cfg2 0.0847 -> 0.0813 ms): the polymul turn pass works on 4-coefficient groups
-  if (p->lazy60 && lazy_enabled()) {
-    if (prefetch_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true, true>(p, out, in, bop, bcast, batch, st);
-    return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true>(p, out, in, bop, bcast, batch, st);
-  }
+  if (p->lazy60 && lazy_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true>(p, out, in, bop, bcast, batch, st);
   return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 
@@ -558,9 +546,9 @@ static rnt_status cluster_op_c(const rnt_plan_s* p, int op, u64* out, const u64*
   }
 }
 
-// Latency cluster kernel (ntt_clat.cuh): E coefficients per thread and C CTAs
-// per limb (defaults in clat_op; env RNT_CLAT_E = 4 / 8 and RNT_CLAT_C = 8 / 16
-// override where the geometry is valid); env RNT_CLAT=0 falls back to k_cluster.
+// Latency cluster kernel (ntt_clat.cuh): E = 4 coefficients per thread and C CTAs
+// per limb (defaults in clat_op; env RNT_CLAT_C = 8 / 16 overrides where the
+// geometry is valid); env RNT_CLAT=0 falls back to k_cluster.
 template <int LOGN, int C, int E, int MODE>
 static rnt_status launch_clat_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                 uint32_t batch, cudaStream_t st) {
@@ -605,24 +593,18 @@ static rnt_status clat_op_ce(const rnt_plan_s* p, int op, u64* out, const u64* i
   }
 }
 
-// Defaults (measured, single-polynomial forward latency under CUDA-graph replay):
+// Defaults (measured, single-polynomial forward latency under CUDA-graph replay;
+// E = 8 coefficients per thread measured slower at every N and is not built):
 // C = 8 up to 2^12, 16 above; E = 4 (2^12 / 2^13 / 2^14 / 2^15: 3.5 / 3.8 / 5.2 / 8.0 us
 // vs 7.5 / 8.1 / 8.2 / 9.4 us for k_cluster).
 template <int LOGN>
 static rnt_status clat_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                           uint32_t batch, cudaStream_t st) {
   constexpr int DC = LOGN <= 12 ? 8 : 16, DE = 4;
-  static const int ce = [] {
-    const int c = env_int("RNT_CLAT_C", DC) == 8 ? 8 : 16;
-    const int e = env_int("RNT_CLAT_E", DE) == 8 ? 8 : 4;
-    return c * 16 + e;
-  }();
-  switch (ce) {
-    case 8 * 16 + 4: if constexpr (clat_valid<LOGN, 8, 4>()) return clat_op_ce<LOGN, 8, 4>(p, op, out, in, bop, bcast, batch, st); break;
-    case 8 * 16 + 8: if constexpr (clat_valid<LOGN, 8, 8>()) return clat_op_ce<LOGN, 8, 8>(p, op, out, in, bop, bcast, batch, st); break;
-    case 16 * 16 + 4: if constexpr (clat_valid<LOGN, 16, 4>()) return clat_op_ce<LOGN, 16, 4>(p, op, out, in, bop, bcast, batch, st); break;
-    case 16 * 16 + 8: if constexpr (clat_valid<LOGN, 16, 8>()) return clat_op_ce<LOGN, 16, 8>(p, op, out, in, bop, bcast, batch, st); break;
-    default: break;
+  static const int c = env_int("RNT_CLAT_C", DC) == 8 ? 8 : 16;
+  if (c != DC) {
+    if (c == 8) { if constexpr (clat_valid<LOGN, 8, DE>()) return clat_op_ce<LOGN, 8, DE>(p, op, out, in, bop, bcast, batch, st); }
+    else { if constexpr (clat_valid<LOGN, 16, DE>()) return clat_op_ce<LOGN, 16, DE>(p, op, out, in, bop, bcast, batch, st); }
   }
   static_assert(clat_valid<LOGN, DC, DE>(), "default latency geometry");
   return clat_op_ce<LOGN, DC, DE>(p, op, out, in, bop, bcast, batch, st);
@@ -764,7 +746,7 @@ template <int LOGN>
 static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                  DigitSpec ds, cudaStream_t st) {
   static const bool cta = env_int("RNT_EXTPROD", 1) != 0;
-  if (cta) {
+  if constexpr (LOGN == 10) if (cta) {
     switch (ds.levels) {
       case 1: return launch_extprod_cta<LOGN, 1>(p, out, c, z, n_slot, ds, st);
       case 2: return launch_extprod_cta<LOGN, 2>(p, out, c, z, n_slot, ds, st);

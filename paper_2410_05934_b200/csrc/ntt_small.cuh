@@ -326,7 +326,7 @@ struct Passes {
 static_assert(Passes<10, 32>::k(2) == 2 && Passes<10, 32>::k(3) == 2 && Passes<10, 32>::s(3) == 8, "split tail");
 static_assert(Passes<10, 3>::k(3) == 1 && Passes<10, 3>::s(3) == 9, "radix-8 schedule");
 
-// SRC0: source of the first pass (kFromGlobal, or kFromBuf after warp_prefetch).
+// SRC0: source of the first pass (kFromGlobal, or kFromBuf for data already staged).
 template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0,
           int SRC0 = kFromGlobal>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
@@ -385,25 +385,8 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // [x * kTeamWarps * P, ...) of limb l; unit (b, l) sits at (b L + l) N
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
-// Stage the warp's polynomials into its (padded) buffer with 8-byte cp.async:
-// every global load of the first pass is in flight at once instead of one
-// group's loads per loop iteration (PF kernels).
-template <int LOGN>
-__device__ __forceinline__ void warp_prefetch(u64* buf, const GView& src, int lane) {
-  constexpr int N = 1 << LOGN;
-#pragma unroll 4
-  for (int j = lane; j < kWarpElems; j += 32) {
-    const int poly = j >> LOGN;
-    if (src.live(poly)) cp_async8(buf + wpad(j), src.at(poly) + (j & (N - 1)));
-  }
-  cp_async_wait_all();
-  __syncwarp();
-}
-
 // LZ: lazy CT ranges (ct_bfly_lz), valid when every modulus of the plan is < 2^60.
-// PF: first pass from shared memory after warp_prefetch (MODE 0, 1, 2).
-template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false,
-          bool PF = false>
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false>
 __global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
@@ -423,9 +406,7 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const GView dst{out + (uint64_t)l * N, p0, stride, B};
   const TW* Tf = tw_fwd + (size_t)l * N;
   const TW* Ti = tw_inv + (size_t)l * N;
-  constexpr bool PFM = PF && MODE != 3;
-  constexpr int SRC0 = PFM ? kFromBuf : kFromGlobal;
-  if constexpr (PFM) warp_prefetch<LOGN>(buf, src, lane);
+  constexpr int SRC0 = kFromGlobal;
   if constexpr (MODE == 0) {
     warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ, 0, SRC0>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {

@@ -428,9 +428,7 @@ print("VARIANT_OK" if ok else "VARIANT_BAD")
                           {"RNT_LAT_UNITS": "0"}, {"RNT_LAT_UNITS": "100000"},
                           {"RNT_LAZY": "0", "RNT_LAT_UNITS": "0"}, {"RNT_LAZY": "0"},
                           {"RNT_LAZY": "0", "RNT_LARGE_VARIANT": "5"},
-                          {"RNT_CLAT": "0"}, {"RNT_CLAT_E": "8"}, {"RNT_CLAT_C": "16"},
-                          {"RNT_PREFETCH": "1", "RNT_LAT_UNITS": "0"},
-                          {"RNT_CLAT_C": "16", "RNT_CLAT_E": "8"}])
+                          {"RNT_CLAT": "0"}, {"RNT_CLAT_C": "8"}, {"RNT_CLAT_C": "16"}])
 def test_kernel_variants(env):
     """Every shipped launch variant (selected by env knobs, read once per process)
     is bit-exact against the oracle."""
