@@ -68,6 +68,16 @@ __device__ __forceinline__ void bfly_v0(u64& X, u64& Y, u64 w, u64 wp, u64 q, u6
   Y = x - T + q2;
 }
 
+// V14: V0 with the kernels' sign-test conditional subtraction (modarith.cuh csub)
+__device__ __forceinline__ void bfly_v14(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
+  const u64 d = X - q2;
+  u64 x = (long long)d < 0 ? X : d;
+  u64 Q = __umul64hi(Y, wp);
+  u64 T = Y * w - Q * q;
+  X = x + T;
+  Y = x - T + q2;
+}
+
 __device__ __forceinline__ void bfly_v2(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 q2, u64 nq) {
   u64 x = X >= q2 ? X - q2 : X;
   u64 Q = hi64_exact(Y, wp);
@@ -259,6 +269,7 @@ __global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long*
       if (V == 7) bfly_v7(X[i], Y[i], w, wp, q2, nq);
       if (V == 8) bfly_v8(X[i], Y[i], w, wp, 4 * q, nq);
       if (V == 9) bfly_v9(X[i], Y[i], w, wp, 4 * q, nq);
+      if (V == 14) bfly_v14(X[i], Y[i], w, wp, q, q2, nq);
     }
   }
   long long t1 = clock64();
@@ -495,6 +506,7 @@ int main() {
   };
   for (int rep = 0; rep < 2; ++rep) {
     run(k_bfly<0>, "V0_nvcc");
+    run(k_bfly<14>, "V14_sign_csub");
     run(k_bfly<2>, "V2_split_exact");
     run(k_bfly<3>, "V3_split_hiword");
     run(k_bfly<4>, "V4_ptx_block");
