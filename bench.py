@@ -465,7 +465,8 @@ def bench_ours(args, wl, parts):
             traffic = json.load(open(prof)).get(f"{wl}:part{dom}")
         except Exception:
             traffic = None
-    kern = f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch)" if s["logn"] <= 10 else \
+    kern = f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes)" \
+        if s["logn"] <= 10 else \
         f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
     # whole step: every butterfly of every part over the timed step time (all ranks)
     step_bfly = sum(2 * st["limbs"] * st["polys"] * (1 << st["logn"]) // 2 * st["logn"] for st in states) * (
