@@ -570,6 +570,21 @@ inline size_t warp_tma_smem_bytes() {
 // digit is formed while the first pass loads c_t; the last forward pass
 // multiplies (Montgomery) and accumulates into two shared-memory accumulators;
 // two inverse transforms (N^{-1} 2^64 scale) write the output pair.
+// Copy the warp's polynomials (padded layout) into buf with 8-byte cp.async:
+// every global load is in flight at once (the external product's warps have
+// only long-latency work in their first pass).
+template <int LOGN>
+__device__ __forceinline__ void warp_stage(u64* buf, const GView& src, int lane) {
+  constexpr int N = 1 << LOGN;
+#pragma unroll 4
+  for (int e = lane; e < kWarpElems; e += 32) {
+    const int poly = e >> LOGN;
+    if (src.live(poly)) cp_async8(buf + wpad(e), src.at(poly) + (e & (N - 1)));
+  }
+  cp_async_wait_all();
+  __syncwarp();
+}
+
 struct DigitSpec {
   uint32_t bg, levels;
   int64_t off;     // sum_{i < l-1} (B/2) B^i
@@ -590,7 +605,9 @@ __device__ __forceinline__ u64 gadget_digit(u64 v, u64 q, const DigitSpec& ds, u
 }
 
 // first forward pass of digit j of component view `src`
-template <int LOGN, int S, int K, bool LZ = false>
+// STAGED: the component was already copied into buf (same padded positions,
+// warp_stage); the digit is formed from shared memory instead of global memory.
+template <int LOGN, int S, int K, bool LZ = false, bool STAGED = false>
 __device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, const TW* T, u64 q, u64 q2,
                                                const DigitSpec& ds, uint32_t j) {
   using Geo = PassGeo<LOGN, S, K>;
@@ -604,7 +621,10 @@ __device__ __forceinline__ void fwd_pass_digit(u64* buf, GView src, int lane, co
     const u64* sp = src.at(g.poly) + jj0;
     u64 x[1 << K];
 #pragma unroll
-    for (int i = 0; i < (1 << K); ++i) x[i] = live ? gadget_digit(sp[i * Geo::LO], q, ds, j) : 0ull;
+    for (int i = 0; i < (1 << K); ++i) {
+      const u64 v = STAGED ? buf[pb + pad_off<LOGN, S, Geo::LO>(i)] : (live ? sp[i * Geo::LO] : 0ull);
+      x[i] = live ? gadget_digit(v, q, ds, j) : 0ull;
+    }
     ct_group<S, K, LZ>(x, T, g.hi, q, q2);
 #pragma unroll
     for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
@@ -710,7 +730,8 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
   {
     const uint32_t t = (uint32_t)warp / LV, j = (uint32_t)warp % LV;
     const GView cv{c + (uint64_t)t * N, s0, 2ull * N, n_slot};
-    fwd_pass_digit<LOGN, 0, PS::k(0), LZ>(buf, cv, lane, tw_fwd, q, q2, ds, j);
+    warp_stage<LOGN>(buf, cv, lane);
+    fwd_pass_digit<LOGN, 0, PS::k(0), LZ, true>(buf, cv, lane, tw_fwd, q, q2, ds, j);
     sfor<1, NP>([&](auto P_) {
       constexpr int p = decltype(P_)::value;
       fwd_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, kToBuf, 0, LZ>(buf, cv, cv, lane, tw_fwd, q, q2);
