@@ -250,12 +250,52 @@ __device__ __forceinline__ void bfly_v9(u64& X, u64& Y, u64 w, u64 wp, u64 q4, u
 
 constexpr int ITERS = 256;
 
+// V15: V14 for a sparse modulus q = 2^60 - 2^b + 1 (1 <= b < 32): Q q mod 2^64 =
+// (Q << 60) - (Q << b) + Q is formed with shifts and adds on the ALU pipe instead of
+// one IMAD.WIDE + two IMAD on the fmaheavy pipe.
+__device__ __forceinline__ void bfly_v15(u64& X, u64& Y, u64 w, u64 wp, u64 q2, int b) {
+  const u64 d = X - q2;
+  u64 x = (long long)d < 0 ? X : d;
+  u64 Q = __umul64hi(Y, wp);
+  const uint32_t Q0 = (uint32_t)Q, Q1 = (uint32_t)(Q >> 32);
+  const u64 Qb = ((u64)__funnelshift_l(Q0, Q1, b) << 32) | (uint32_t)(Q0 << b);   // Q << b (b < 32)
+  const u64 Q60 = (u64)(Q0 << 28) << 32;                                            // Q << 60 mod 2^64
+  u64 T = Y * w - Q - Q60 + Qb;
+  X = x + T;
+  Y = x - T + q2;
+}
+
+// V16: V15 with the correction neg = (Q << b) - Q - (Q << 60) formed first (runtime shift
+// counts, so ptxas cannot turn the shifts into IMADs by constants) and folded into the
+// addend of the y w product.
+__device__ __forceinline__ void bfly_v16(u64& X, u64& Y, u64 w, u64 wp, u64 q2, int b, int s28) {
+  const u64 d = X - q2;
+  u64 x = (long long)d < 0 ? X : d;
+  u64 Q = __umul64hi(Y, wp);
+  const uint32_t Q0 = (uint32_t)Q, Q1 = (uint32_t)(Q >> 32);
+  uint32_t n0, n1;
+  asm("{\n\t.reg .u32 t0, t1, t2;\n\t"
+      "shl.b32 t0, %2, %4;\n\t"
+      "shf.l.wrap.b32 t1, %2, %3, %4;\n\t"
+      "shl.b32 t2, %2, %5;\n\t"
+      "sub.cc.u32 %0, t0, %2;\n\t"
+      "subc.u32 %1, t1, %3;\n\t"
+      "sub.u32 %1, %1, t2;\n\t}"
+      : "=r"(n0), "=r"(n1) : "r"(Q0), "r"(Q1), "r"(b), "r"(s28));
+  const u64 neg = ((u64)n1 << 32) | n0;
+  u64 T = Y * w + neg;
+  X = x + T;
+  Y = x - T + q2;
+}
+
 template <int V>
 __global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long* cyc) {
   u64 X[4], Y[4];
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int i = 0; i < 4; ++i) { X[i] = in[gid * 8 + 2 * i]; Y[i] = in[gid * 8 + 2 * i + 1]; }
   const u64 q2 = 2 * q, nq = 0ull - q;
+  const int sb = __ffsll((long long)((1ull << 60) + 1 - q)) - 1;   // V15: q = 2^60 - 2^sb + 1
+  const int s28 = 28 + (int)(q >> 63);                              // V16: runtime 28
   long long t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
@@ -270,6 +310,8 @@ __global__ void k_bfly(u64* out, const u64* in, u64 w, u64 wp, u64 q, long long*
       if (V == 8) bfly_v8(X[i], Y[i], w, wp, 4 * q, nq);
       if (V == 9) bfly_v9(X[i], Y[i], w, wp, 4 * q, nq);
       if (V == 14) bfly_v14(X[i], Y[i], w, wp, q, q2, nq);
+      if (V == 15) bfly_v15(X[i], Y[i], w, wp, q2, sb);
+      if (V == 16) bfly_v16(X[i], Y[i], w, wp, q2, sb, s28);
     }
   }
   long long t1 = clock64();
@@ -507,6 +549,8 @@ int main() {
   for (int rep = 0; rep < 2; ++rep) {
     run(k_bfly<0>, "V0_nvcc");
     run(k_bfly<14>, "V14_sign_csub");
+    run(k_bfly<15>, "V15_sparse_q");
+    run(k_bfly<16>, "V16_sparse_q_alu");
     run(k_bfly<2>, "V2_split_exact");
     run(k_bfly<3>, "V3_split_hiword");
     run(k_bfly<4>, "V4_ptx_block");

@@ -22,7 +22,10 @@ KEYS = {
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-    "fmaheavy_pipe_pct": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    # ncu 2025 exposes the fmaheavy pipe only as ..._elapsed (the _active form is absent)
+    "fmaheavy_pipe_pct": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "fmaheavy_inst_pct": "sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_elapsed",
+    "elapsed_cycles": "sm__cycles_elapsed.avg",
     "inst_executed": "smsp__inst_executed.sum",
     "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -78,6 +81,10 @@ def main():
                 elif name == "sm_mhz":
                     v = scale(v, u.get(key, ""), "MHz")
                 k[name] = v
+            # every fmaheavy / fma / alu pipe counter the report holds (names vary by ncu version)
+            k["pipes"] = {key: fnum(val) for key, val in d.items()
+                          if ("pipe_fmaheavy" in key or "pipe_alu" in key or "pipe_fma_" in key)
+                          and fnum(val) is not None}
             stalls = {}
             for key, val in d.items():
                 if key.startswith("smsp__average_warps_issue_stalled_") and key.endswith("_per_issue_active.ratio"):
