@@ -69,6 +69,7 @@ def _load():
                 "or_decompose": (None, [_u64p, u64, u64, u32, u32]),
                 "or_external_product": (None, [_u64p, _u64p, _u64p, u32, u64, u64, u32, u32]),
                 "or_bconv": (None, [_u64p, _u64p, u64, _u64p, u32, _u64p, u32]),
+                "or_hrf_matvec": (None, [_u64p, _u64p, _u64p, _u64p, u32, _u64p, u32, u64]),
                 "or_keyswitch": (None, [_u64p, _u64p, _u64p, _u64p, u32, _u64p, u32, _u64p, u32, u32]),
                 "or_batch": (i32, [i32, _u64p, _u64p, i32, u32, u32, u32, _u64p, _u64p, i32]),
             }
@@ -225,6 +226,29 @@ def external_product(c, rgsw_hat, q: int, psi: int, base_log2: int, levels: int)
     _check_canonical(c, q)
     out = np.zeros_like(c)
     _load().or_external_product(_p(out), _p(c), _p(z), n.bit_length() - 1, q, psi, base_log2, levels)
+    return out
+
+
+def hrf_matvec(pt, ct, moduli, add=None) -> np.ndarray:
+    """HRF-MatVec (tab:repack): out[c][l] = add[c][l] + sum_j pt[j][l] (.) ct[j][c][l]
+    mod q_l, NTT form.  pt [n_slot][L][N], ct [n_slot][2][L][N], add [2][L][N] or None."""
+    pt = np.ascontiguousarray(pt, dtype=np.uint64)
+    ct = np.ascontiguousarray(ct, dtype=np.uint64)
+    ns, L, n = pt.shape
+    assert ct.shape == (ns, 2, L, n)
+    qs = _vec(moduli)
+    assert qs.size == L
+    for l in range(L):
+        _check_canonical(pt[:, l], int(qs[l]))
+        _check_canonical(ct[:, :, l], int(qs[l]))
+    a = None
+    if add is not None:
+        a = np.ascontiguousarray(add, dtype=np.uint64)
+        assert a.shape == (2, L, n)
+        for l in range(L):
+            _check_canonical(a[:, l], int(qs[l]))
+    out = np.zeros((2, L, n), dtype=np.uint64)
+    _load().or_hrf_matvec(_p(out), _p(pt), _p(ct), _p(a) if a is not None else None, ns, _p(qs), L, n)
     return out
 
 

@@ -313,6 +313,31 @@ void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_
   free(fwd); free(inv); free(acc); free(dig); free(tmp);
 }
 
+/* HRF-MatVec, the homomorphic-rotation-free matrix-vector product of repack
+ * (tab:repack P:393-395, row HRF-MatVec: 0 rotations, n_slot scalar
+ * multiplications, n_slot precomputed rotation ciphertexts).
+ * With every rotation ciphertext ct_j = rot_j(Enc(s)) precomputed and every
+ * plaintext diagonal pt_j (giant-step automorph already applied) in
+ * NTT form, the linear transformation is a sum of scalar (plaintext-ciphertext)
+ * products, per RNS limb l, component c and NTT slot k (reading H1):
+ *   out[c][l][k] = add[c][l][k] + sum_{j < n_slot} pt[j][l][k] * ct[j][c][l][k]  mod q_l
+ * pt [n_slot][L][N], ct [n_slot][2][L][N], add [2][L][N] or NULL (the "+ b" of
+ * As + b), out [2][L][N]. */
+void or_hrf_matvec(uint64_t* out, const uint64_t* pt, const uint64_t* ct, const uint64_t* add, uint32_t n_slot,
+                   const uint64_t* q, uint32_t L, uint64_t n) {
+  for (uint32_t c = 0; c < 2; ++c)
+    for (uint32_t l = 0; l < L; ++l)
+      for (uint64_t k = 0; k < n; ++k) {
+        uint64_t acc = add ? add[((uint64_t)c * L + l) * n + k] % q[l] : 0;
+        for (uint32_t j = 0; j < n_slot; ++j) {
+          uint64_t a = pt[((uint64_t)j * L + l) * n + k];
+          uint64_t b = ct[(((uint64_t)j * 2 + c) * L + l) * n + k];
+          acc = or_addmod(acc, or_mulmod(a, b, q[l]), q[l]);
+        }
+        out[((uint64_t)c * L + l) * n + k] = acc;
+      }
+}
+
 /* Fast basis conversion BConv (CKKS key switching ModUp / ModDown, P:247-248;
  * SPEC S:82-90): from basis Q = {q_0..q_{L-1}} to P = {p_0..p_{K-1}},
  * per coefficient (reading G3):

@@ -30,6 +30,8 @@ void or_automorph(uint64_t* out, const uint64_t* a, uint32_t logn, uint64_t q, u
 void or_decompose(uint64_t* digits, uint64_t v, uint64_t q, uint32_t base_log2, uint32_t levels);
 void or_external_product(uint64_t* out, const uint64_t* c, const uint64_t* rgsw_hat, uint32_t logn, uint64_t q,
                          uint64_t psi, uint32_t base_log2, uint32_t levels);
+void or_hrf_matvec(uint64_t* out, const uint64_t* pt, const uint64_t* ct, const uint64_t* add, uint32_t n_slot,
+                   const uint64_t* q, uint32_t L, uint64_t n);
 void or_bconv(uint64_t* out, const uint64_t* in, uint64_t n, const uint64_t* q, uint32_t L, const uint64_t* p,
               uint32_t K);
 void or_keyswitch(uint64_t* out, const uint64_t* d, const uint64_t* evk, const uint64_t* add0, uint32_t logn,
