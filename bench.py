@@ -12,19 +12,31 @@ the metric names both halves of: N=2^16 x 45 limbs (CKKS) plus N=2^10 x 16384
 polynomials (TFHE).  `value` counts limb-transforms (one forward or one
 inverse N-point transform of one limb) per second over all ranks.
 
-Multi-GPU (torchrun): weak scaling by default -- rank r owns polynomial
-batch index r of the global problem (inputs generated from the global
-counters, so shards are slices of one global array); no collective touches
-the data path.  Timing: per-step CUDA events on the launching stream with an
-L2 flush (256 MiB write) between steps outside the events, W warm-up steps,
+Multi-GPU: `--gpus N` (N > 1) re-launches this script as N NCCL ranks
+through torch.distributed.run unless it already runs under torchrun.  The
+default for N > 1 is strong scaling: the fixed workload is split by limb and
+polynomial with the weighted contiguous planner of SURVEY §8(e)
+(paper_2410_05934_b200.shard); `--scaling weak` gives rank r polynomial block r
+of a global problem of N copies.  Inputs are generated per shard from global
+counters, so shards are slices of one global array; no collective touches the
+data path.  After the timed region every rank digests its CUDA outputs per
+unit, the digests are all-gathered and rank 0 compares their hash with the
+oracle-computed hash in tests/golden/bench_digests.json (`digests_ok`).  For
+N > 1 an `e2e_nccl` block times rank 0 scattering the inputs over NCCL, the
+sharded compute, and the gather of the outputs back to rank 0.
+Timing: per-step CUDA events on the launching stream with an L2 flush
+(>= 512 MiB write) between steps outside the events, W warm-up steps,
 barrier + synchronize around the timed region, max over ranks.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -54,7 +66,7 @@ WORKLOADS = {
              "parts": [(16, 45, 1, 0), (10, 1, 16384, 0)]},
 }
 
-L2_FLUSH_BYTES = 256 << 20
+L2_FLUSH_BYTES = 512 << 20   # >= 4x the 126 MB L2 (SURVEY §8(d) timing protocol)
 SPIN_CYCLES = 100_000   # ~50 us at 1.965 GHz
 FMA_SLOTS_PER_BFLY = 16   # exact Shoup butterfly: 6 wide/hi multiplies x 2 + 4 IMAD
 IMAD_SLOTS_PER_CLK_SM = 64
@@ -205,12 +217,19 @@ def run_oracle_sample(parts, poly_offset: int, cores: int, min_seconds: float):
     return reps, el
 
 
-def cpu_baseline_block(wl, parts, cores, min_seconds=8.0):
+def cpu_baseline_block(wl, parts, cores, min_seconds=8.0, single_seconds=4.0):
+    """The oracle as it stands on the host: all cores (the pthread pool over units)
+    on the full workload, and one thread on a 1/64 sample."""
     reps, el = run_oracle_sample(parts, 0, cores, min_seconds)
     per = transforms_per_step(parts)
-    return {"value": per * reps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+    small = reference_sample(parts, 64)
+    reps1, el1 = run_oracle_sample(small, 0, 1, single_seconds)
+    per1 = transforms_per_step(small)
+    return {"value": per * reps / el, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"full {wl} workload x {reps} repetition(s) ({per} limb-transforms each, "
-                      f"{el:.1f} s wall on {cores} threads; oracle = plain C, exact 128-bit %)"}
+                      f"{el:.1f} s wall on {cores} threads; oracle = plain C, exact 128-bit %)",
+            "single_thread": {"value": per1 * reps1 / el1, "unit": UNIT, "cores": 1,
+                              "sample": f"1/64 of {wl} ({per1} limb-transforms) x {reps1}, {el1:.1f} s on 1 thread"}}
 
 
 def reference_sample(parts, frac: int = 8):
@@ -265,6 +284,93 @@ def bench_reference(args, wl, parts):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------ sharding + digests
+GOLDEN_DIGESTS = os.path.join(ROOT, "tests", "golden", "bench_digests.json")
+
+
+def plan_blocks(parts, ws: int, rank: int, scaling: str):
+    """The blocks of the global job that `rank` owns.
+
+    strong: the fixed workload is split by limb x polynomial with the weighted
+    contiguous planner (paper_2410_05934_b200.shard, pure Python).  weak: rank r
+    owns polynomial block r of a global problem of `ws` copies of the workload.
+    A block is a dict: part index, log2n, the block's moduli, its global limb
+    offset / total limbs, its polynomial count and global polynomial offset, seed.
+    """
+    from paper_2410_05934_b200 import shard as shd
+
+    out = []
+    if scaling == "weak":
+        for pi, (logn, limbs, polys, seed) in enumerate(parts):
+            out.append(dict(part=pi, logn=logn, mods=primes_for(logn, limbs), loff=0, ltot=limbs, polys=polys,
+                            poff=rank * polys, seed=seed))
+    else:
+        sp = [shd.Part(lg, lm, po) for (lg, lm, po, _) in parts]
+        for b in shd.plan(sp, ws)[rank]:
+            logn, limbs, polys, seed = parts[b.part]
+            out.append(dict(part=b.part, logn=logn, mods=primes_for(logn, limbs)[b.limb_begin:b.limb_end],
+                            loff=b.limb_begin, ltot=limbs, polys=b.poly_end - b.poly_begin, poff=b.poly_begin,
+                            seed=seed))
+    return out
+
+
+def block_inputs(blk):
+    """(a, b_hat) of a block: [polys][limbs][N] uint64 slices of the global arrays."""
+    n = 1 << blk["logn"]
+    a = inputs.residues_limbs(blk["seed"], blk["polys"], blk["mods"], n, blk["loff"], blk["ltot"],
+                              batch_offset=blk["poff"])
+    bh = inputs.residues_limbs(blk["seed"] + 1, blk["polys"], blk["mods"], n, blk["loff"], blk["ltot"],
+                               batch_offset=blk["poff"])
+    return a, bh
+
+
+def block_digests(blk, c: np.ndarray):
+    """Per-unit digest rows (part, global poly, global limb, sum, wsum) of a block's output."""
+    rows = []
+    for i in range(c.shape[0]):
+        for j in range(c.shape[1]):
+            s_, w_ = inputs.digest(c[i, j])
+            rows.append((blk["part"], blk["poff"] + i, blk["loff"] + j, s_, w_))
+    return rows
+
+
+def gather_rows(rows, ws: int):
+    """All-gather every rank's digest rows (any backend); every rank gets the union."""
+    if ws == 1:
+        return list(rows)
+    import torch.distributed as dist
+
+    got = [None] * ws
+    dist.all_gather_object(got, list(rows))
+    return [r for g in got for r in g]
+
+
+def digests_sha(rows) -> str:
+    arr = np.array(sorted(rows), dtype=np.uint64)
+    return hashlib.sha256(arr.tobytes()).hexdigest()
+
+
+def check_digests(wl: str, rows):
+    """Compare the gathered digests with the oracle's (tests/golden, written by
+    tools/make_golden_digests.py from oracle/ only).  None if no golden entry."""
+    if not os.path.exists(GOLDEN_DIGESTS):
+        return None
+    g = json.load(open(GOLDEN_DIGESTS)).get(wl)
+    if g is None:
+        return None
+    return len(rows) == g["units"] and digests_sha(rows) == g["sha256"]
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # --------------------------------------------------------------------- ours
 def bench_ours(args, wl, parts):
     import torch
@@ -272,33 +378,33 @@ def bench_ours(args, wl, parts):
     import paper_2410_05934_b200 as R
 
     ws, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
+    # RNT_BENCH_SHARE_GPU=1 (testing the multi-rank path on a 1-GPU box only): ranks
+    # share the visible GPUs and talk over gloo; never used for a reported number
+    share = os.environ.get("RNT_BENCH_SHARE_GPU") == "1"
+    if local >= ndev and not share:
+        raise SystemExit(f"bench.py: local rank {local} but only {ndev} visible GPU(s)")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = "gloo" if share else "nccl"
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
 
-    # ---- shard.  weak: rank r owns global polynomial block r of every part.
-    # strong: the fixed global job is split by limb x polynomial with the
-    # weighted contiguous planner of SURVEY §8(e) (paper_2410_05934_b200.shard).
-    from paper_2410_05934_b200 import shard as shd
-
-    blocks = []   # (log2n, limbs_slice_mods, limb_offset, total_limbs, polys, poly_offset, seed)
-    if args.scaling == "weak":
-        for (logn, limbs, polys, seed) in parts:
-            blocks.append((logn, primes_for(logn, limbs), 0, limbs, polys, rank * polys, seed))
-    else:
-        sp = [shd.Part(lg, lm, po) for (lg, lm, po, _) in parts]
-        for b in shd.plan(sp, ws)[rank]:
-            logn, limbs, polys, seed = parts[b.part]
-            mods = primes_for(logn, limbs)[b.limb_begin:b.limb_end]
-            blocks.append((logn, mods, b.limb_begin, limbs, b.poly_end - b.poly_begin, b.poly_begin, seed))
+    # ---- shard (plan_blocks): strong = the fixed workload split by limb x polynomial,
+    # weak = rank r owns polynomial block r of ws copies
+    blocks = plan_blocks(parts, ws, rank, args.scaling)
     states = []
-    for (logn, mods, loff, ltot, polys, poff, seed) in blocks:
-        a = inputs.residues_limbs(seed, polys, mods, 1 << logn, loff, ltot, batch_offset=poff)
-        bhat = inputs.residues_limbs(seed + 1, polys, mods, 1 << logn, loff, ltot, batch_offset=poff)
+    for blk in blocks:
+        a, bhat = block_inputs(blk)
+        logn, mods = blk["logn"], blk["mods"]
         plan = R.Plan(logn, mods, device=local)
         da = torch.from_numpy(a.view(np.int64)).to(dev)
         db = torch.from_numpy(bhat.view(np.int64)).to(dev)
@@ -307,8 +413,8 @@ def bench_ours(args, wl, parts):
         # two output / workspace sets: consecutive e2e steps alternate between them
         hc = [torch.empty_like(ha).pin_memory() for _ in range(2)]
         ws_buf = [torch.empty_like(da) for _ in range(2)]
-        states.append(dict(logn=logn, limbs=len(mods), polys=polys, plan=plan, a=da, b=db, c=dc,
-                           ha=ha, hc=hc, ws=ws_buf))
+        states.append(dict(logn=logn, limbs=len(mods), polys=blk["polys"], plan=plan, a=da, b=db, c=dc,
+                           ha=ha, hc=hc, ws=ws_buf, blk=blk))
     # the dominant kernel: largest butterfly count part
     work = [(2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]) for s in states]
     dom = int(np.argmax(work)) if work else 0
@@ -320,24 +426,25 @@ def bench_ours(args, wl, parts):
     run_streams = [torch.cuda.Stream() for _ in states] if concurrent else [stream for _ in states]
     seq_streams = [stream for _ in states]
 
-    def step(ev=None, span=None, streams=None):
+    def step(ev=None, span=None, streams=None, base=None):
+        base = stream if base is None else base
         streams = run_streams if streams is None else streams
         if span is not None:
-            span[0].record(stream)
+            span[0].record(base)
         for i, s in enumerate(states):
             rs = streams[i]
-            if rs is not stream:
-                rs.wait_stream(stream)
+            if rs is not base:
+                rs.wait_stream(base)
             if ev is not None:
                 ev[i][0].record(rs)
             R.polymul(s["plan"], s["c"], s["a"], s["b"], b_is_eval=True, stream=rs)
             if ev is not None:
                 ev[i][1].record(rs)
         for rs in streams:
-            if rs is not stream:
-                stream.wait_stream(rs)
+            if rs is not base:
+                base.wait_stream(rs)
         if span is not None:
-            span[1].record(stream)
+            span[1].record(base)
 
     # end to end: each part on its own user stream (independent batches overlap
     # their PCIe traffic); the library pipelines chunks inside each call.  Step k
@@ -396,7 +503,9 @@ def bench_ours(args, wl, parts):
     # region overlaps them, so each part is also timed alone (one stream, L2
     # flushed, same spin) in a short sequential pass
     part_ms_seq = part_ms
-    if concurrent:
+    # collective on every rank (barriers inside) whenever the workload has several
+    # parts -- a rank whose shard holds one part still takes part in the barriers
+    if args.concurrent_parts and len(parts) > 1:
         nseq = min(args.steps, 20)
         sevs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in states] for _ in range(nseq)]
         barrier()
@@ -414,6 +523,37 @@ def bench_ours(args, wl, parts):
         step(None, sp)
     barrier()
     warm_ms = statistics.mean(sp[0].elapsed_time(sp[1]) for sp in warm_spans)
+
+    # ---- secondary: the step captured once in a CUDA graph and replayed (no host
+    # launch work per step), L2 flushed between replays like the timed region
+    graph = None
+    if args.graph and states:
+        try:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            gstreams = [torch.cuda.Stream() for _ in states] if concurrent else [cap for _ in states]
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    step(None, None, gstreams, base=cap)
+            stream.wait_stream(cap)
+            gspans = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(min(args.steps, 50))]
+            barrier()
+            for sp in gspans:
+                flush.zero_()
+                torch.cuda._sleep(SPIN_CYCLES)
+                sp[0].record(stream)
+                g.replay()
+                sp[1].record(stream)
+            barrier()
+            gms = [sp[0].elapsed_time(sp[1]) for sp in gspans]
+            local_xf = sum(2 * st["limbs"] * st["polys"] for st in states)
+            graph = {"ms_per_step": statistics.mean(gms), "median": statistics.median(gms),
+                     "rank0_value": local_xf / (statistics.mean(gms) * 1e-3), "unit": UNIT,
+                     "note": "secondary, rank 0: one step captured in a CUDA graph, replayed; L2 flushed"}
+            del g
+        except Exception as e:   # capture is an optional measurement; report why it is absent
+            graph = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
     e2e_ms = float("nan")
@@ -438,8 +578,33 @@ def bench_ours(args, wl, parts):
         e2e_ms = e0.elapsed_time(e1)
     h2d = sum(s["a"].numel() * 8 for s in states)
 
+    # ---- correctness of what was timed: per-unit digests of every rank's CUDA
+    # outputs, all-gathered; rank 0 compares their hash with the oracle's
+    # (tests/golden/bench_digests.json, written from oracle/ only)
+    rows = []
+    for st in states:
+        rows += block_digests(st["blk"], st["c"].cpu().numpy().view(np.uint64))
+    all_rows = gather_rows(rows, ws)
+    digests_ok = check_digests(wl, all_rows) if (args.scaling == "strong" or ws == 1) else None
+    e2e_match = None
+    if args.e2e:   # the host-buffer path returned the same outputs as the device path
+        last = (args.steps - 1) % 2 if args.e2e_overlap else 0
+        e2e_match = all(torch.equal(st["hc"][last], st["c"].cpu()) for st in states)
+
+    # ---- N > 1: end to end over NCCL (rank 0 scatters the inputs, gathers the outputs)
+    nccl = None
+    if ws > 1 and args.nccl_e2e and args.scaling == "strong" and backend == "nccl":
+        nccl = scatter_gather_e2e(args, wl, parts, ws, rank, dev, stream, states, R, barrier)
+
+    # distinct physical GPUs that ran a shard (device UUIDs gathered from every rank)
+    try:
+        my_gpu = str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        my_gpu = f"{socket.gethostname()}:{local}"
+    gpus_active = len(set(gather_rows([my_gpu], ws)))
+
     # ---- max over ranks
-    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=red_dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     total_ms, e2e_ms = float(t[0]), float(t[1])
@@ -456,7 +621,7 @@ def bench_ours(args, wl, parts):
     peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9   # Gbfly/s
     s = states[dom]
     bfly_launch = 2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]
-    dom_ms = statistics.mean(part_ms_seq[dom])
+    dom_ms = statistics.mean(part_ms_seq[dom])   # rank 0's dominant kernel
     achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -497,11 +662,19 @@ def bench_ours(args, wl, parts):
             "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded SplitMix64 uniform residues mod 60-bit NTT primes)",
             "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}",
-                       "l2": "flushed (256 MiB write) between steps, outside the timed events",
+                       "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) between steps, outside the timed events",
                        "launch": "a ~50 us device spin precedes each step's start event (outside the events): "
                                  "the events time device execution, not host launch latency",
                        "global_polys_per_part": [p[2] * (ws if args.scaling == 'weak' else 1) for p in parts],
-                       "parallelism": f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws}, no data-path collective"},
+                       "parallelism": (f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws} "
+                                       f"({'N copies of the workload' if args.scaling == 'weak' else 'the fixed workload split by shard.plan'}), "
+                                       "no data-path collective")},
+            "gpus_active": gpus_active,
+            "process_group": backend if ws > 1 else None,
+            "digests_ok": digests_ok,
+            "digests": {"units": len(all_rows), "sha256": digests_sha(all_rows)[:16],
+                        "against": "tests/golden/bench_digests.json (CPU oracle, tools/make_golden_digests.py)",
+                        "e2e_outputs_equal_device_outputs": e2e_match},
             "gpu_launches": launches,
             "step_ms": {"mean": total_ms / args.steps, "median": statistics.median(step_ms), "min": min(step_ms),
                         "p90": sorted(step_ms)[int(0.9 * (len(step_ms) - 1))]},
@@ -517,13 +690,94 @@ def bench_ours(args, wl, parts):
                                  "behind step k's") if args.e2e_overlap else "serial: each step joins before the next"},
             "clocks": clk.summary(),
         }
-        if args.cpu_baseline and ws >= 1 and rank == 0 and (ws == 1):
+        if graph is not None:
+            line["cuda_graph"] = graph
+        if nccl is not None:
+            line["e2e_nccl"] = nccl
+        if args.cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_block(wl, parts, cpu_cores())
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
+
+
+def scatter_gather_e2e(args, wl, parts, ws, rank, dev, stream, states, R, barrier):
+    """N > 1, strong split: rank 0 holds the global inputs of every part on its GPU,
+    scatters each rank's blocks over NCCL, every rank runs its polymuls, and the
+    outputs are gathered back into rank 0's global arrays (NCCL only
+    where a benchmark moves data).  Device time per step on each rank (CUDA events
+    on the launching stream; the NCCL kernels are ordered against it), max over
+    ranks by the caller's reduction below; rank 0 checks the gathered outputs'
+    digests against the oracle's."""
+    import torch
+    import torch.distributed as dist
+
+    layouts = [plan_blocks(parts, ws, r, "strong") for r in range(ws)]
+    sizes = [sum(b["polys"] * len(b["mods"]) << b["logn"] for b in lay) for lay in layouts]
+    mx = max(sizes)
+    buf = torch.empty(mx, dtype=torch.int64, device=dev)
+    glob = out = send = gath = None
+    if rank == 0:
+        glob = [torch.from_numpy(inputs.residues(seed, polys, primes_for(logn, limbs), 1 << logn).view(np.int64)).to(dev)
+                for (logn, limbs, polys, seed) in parts]
+        out = [torch.empty_like(g) for g in glob]
+        send = [torch.empty(mx, dtype=torch.int64, device=dev) for _ in range(ws)]
+        gath = [torch.empty(mx, dtype=torch.int64, device=dev) for _ in range(ws)]
+
+    def slices(r, arrays, flat):
+        off = 0
+        for b in layouts[r]:
+            g = arrays[b["part"]][b["poff"]:b["poff"] + b["polys"], b["loff"]:b["loff"] + len(b["mods"])]
+            n = g.numel()
+            yield g, flat[off:off + n].view(g.shape)
+            off += n
+
+    def one_step():
+        if rank == 0:
+            for r in range(ws):
+                for g, f in slices(r, glob, send[r]):
+                    f.copy_(g)
+        dist.scatter(buf, send if rank == 0 else None, src=0)
+        off = 0
+        for st in states:
+            n = st["a"].numel()
+            st["a"].view(-1).copy_(buf[off:off + n])
+            R.polymul(st["plan"], st["c"], st["a"], st["b"], b_is_eval=True, stream=stream)
+            buf[off:off + n].copy_(st["c"].view(-1))
+            off += n
+        dist.gather(buf, gath if rank == 0 else None, dst=0)
+        if rank == 0:
+            for r in range(ws):
+                for g, f in slices(r, out, gath[r]):
+                    g.copy_(f)
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    res = {"value": transforms_per_step(parts) / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+           "bytes_scattered_per_step": sum(sizes) * 8, "bytes_gathered_per_step": sum(sizes) * 8,
+           "note": "rank 0's device-resident global inputs scattered over NCCL, sharded polymul, outputs "
+                   "gathered to rank 0 (dist.scatter / dist.gather); device time, max over ranks"}
+    if rank == 0:
+        rows = []
+        for pi, o in enumerate(out):
+            h = o.cpu().numpy().view(np.uint64)
+            blk = dict(part=pi, poff=0, loff=0)
+            rows += block_digests(blk, h)
+        res["digests_ok"] = check_digests(wl, rows)
+    return res
 
 
 # Paper-comparable single-polynomial latency (SURVEY §8(f) f3): one 56-bit prime
@@ -697,6 +951,66 @@ def bench_extprod(args):
                                        "sample": "64 slots, single thread"}}), flush=True)
 
 
+def bench_hrf(args):
+    """HRF-MatVec of repack (tab:repack): out = add + sum_j pt_j (.) ct_j
+    over n_slot precomputed rotation ciphertexts, NTT form, at N = 2^16 with 4 limbs (reading
+    H2) and the paper's n_slot = 64 / 256 / 1024 (tab:sw).  HBM-bound: roofline = measured HBM
+    bandwidth; algorithmic bytes = 24 n_slot L N (pt + both ct components read once) + 32 L N
+    (add read, out written).  L2 flushed between steps (the inputs exceed L2 anyway)."""
+    import torch
+
+    import paper_2410_05934_b200 as R
+
+    torch.cuda.set_device(0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    logn, L = 16, 4
+    n = 1 << logn
+    mods = primes_for(logn, L)
+    plan = R.Plan(logn, mods)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    res = {}
+    for n_slot in (64, 256, 1024):
+        pt = torch.from_numpy(inputs.residues(0, n_slot, mods, n).view(np.int64)).cuda()
+        ct = torch.from_numpy(inputs.residues(1, 2 * n_slot, mods, n).view(np.int64)).cuda()
+        add = torch.from_numpy(inputs.residues(2, 2, mods, n).view(np.int64)).cuda()
+        out = torch.empty_like(add)
+        for _ in range(args.warmup):
+            R.hrf_matvec(plan, out, pt, ct, add=add)
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            R.hrf_matvec(plan, out, pt, ct, add=add)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = statistics.mean(ms)
+        alg = (24 * n_slot * L * n + 32 * L * n)
+        gbs = alg / (t * 1e-3) / 1e9
+        res[str(n_slot)] = {"ms": t, "ms_min": min(ms), "GBps": gbs, "frac_hbm": gbs / hbm,
+                            "scalar_mults_per_s": 2 * n_slot * L * n / (t * 1e-3), "alg_bytes": alg}
+        del pt, ct
+        torch.cuda.empty_cache()
+    # CPU oracle on a bounded sample: n_slot = 8, one limb
+    import oracle as O
+
+    pt = inputs.residues(0, 8, mods[:1], n)
+    ct = inputs.residues(1, 16, mods[:1], n).reshape(8, 2, 1, n)
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 3.0:
+        O.hrf_matvec(pt, ct, mods[:1])
+        reps += 1
+    cpu = reps * 2 * 8 * n / (time.perf_counter() - t0)
+    print(json.dumps({"mode": "hrf_matvec", "metric": "HRF-MatVec HBM GB/s (N=2^16, 4 limbs)",
+                      "roofline": {"bound": "hbm", "peak": hbm, "unit": "GB/s"}, "results": res,
+                      "cpu_baseline": {"value": cpu, "unit": "scalar modmults/s", "cores": 1, "kind": "oracle",
+                                       "sample": "n_slot 8, one limb, N=2^16, single thread"}}), flush=True)
+
+
 def bench_modup(args):
     """CKKS ModUp of one key-switching digit at N=2^16 (dnum = 3 for L = 45:
     a 15-limb digit extended to the other 30 limbs + 15 special primes):
@@ -813,6 +1127,59 @@ def bench_keyswitch(args):
                       "results": res}), flush=True)
 
 
+def free_port() -> int:
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def relaunch_cmd(n: int, argv) -> list:
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+
+
+def relaunch(n: int, argv) -> int:
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(relaunch_cmd(n, argv), env=env)
+
+
+def launch_check(args):
+    """The multi-rank plumbing of bench_ours without a GPU: gloo process group,
+    shard plan, per-shard input generation, digest all-gather, max-over-ranks
+    reduction.  Digests are of the generated INPUTS (no method arithmetic), and
+    rank 0 compares them with those of the unsharded inputs."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    parts = WORKLOADS[args.workload]["parts"]
+    rows = []
+    for blk in plan_blocks(parts, ws, rank, args.scaling):
+        a, _ = block_inputs(blk)
+        rows += block_digests(blk, a)
+    all_rows = gather_rows(rows, ws)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        want = []
+        glob_ws = ws if args.scaling == "weak" else 1
+        for pi, (logn, limbs, polys, seed) in enumerate(parts):
+            blk = dict(part=pi, logn=logn, mods=primes_for(logn, limbs), loff=0, ltot=limbs,
+                       polys=polys * glob_ws, poff=0, seed=seed)
+            want += block_digests(blk, block_inputs(blk)[0])
+        print(json.dumps({"launch_check": True, "n_gpus": ws, "scaling": args.scaling, "units": len(all_rows),
+                          "digests_match": digests_sha(all_rows) == digests_sha(want), "max_rank": float(t[0])}),
+              flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -820,7 +1187,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="strong (default): the fixed workload split over the ranks; weak: N copies")
+    ap.add_argument("--no-nccl-e2e", dest="nccl_e2e", action="store_false",
+                    help="N > 1: skip the NCCL scatter / gather end-to-end block")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="skip the CUDA-graph replay block")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="(tests) run the multi-rank launcher, shard plan and digest gather on CPU/gloo; "
+                         "digests of the generated inputs, no compute")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
     ap.add_argument("--e2e-serial", dest="e2e_overlap", action="store_false",
@@ -834,9 +1208,18 @@ def main():
     ap.add_argument("--extprod", action="store_true", help="SURVEY f1 TFHE external product mode")
     ap.add_argument("--modup", action="store_true", help="SURVEY f2 CKKS ModUp (INTT -> BConv -> NTT) mode")
     ap.add_argument("--keyswitch", action="store_true", help="SURVEY f2 CKKS key switch / HROT mode")
+    ap.add_argument("--hrf", action="store_true", help="SURVEY f4 HRF-MatVec scalar multiply-accumulate mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.scaling is None:
+        args.scaling = "strong"
+    single = args.latency or args.automorph or args.extprod or args.modup or args.keyswitch or args.hrf
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours" and not single:
+        # one process per GPU: re-launch this script under torch.distributed.run
+        sys.exit(relaunch(args.gpus, sys.argv[1:]))
+    if args.launch_check:
+        return launch_check(args)
     wl = args.workload
     parts = WORKLOADS[wl]["parts"]
     if args.latency:
@@ -849,6 +1232,8 @@ def main():
         bench_modup(args)
     elif args.keyswitch:
         bench_keyswitch(args)
+    elif args.hrf:
+        bench_hrf(args)
     elif args.impl == "reference":
         bench_reference(args, wl, parts)
     else:

@@ -59,6 +59,16 @@ typedef enum {
  * the device first, synchronise `stream`, and return RNT_E_INVALID_ARG (no
  * output written) if any residue is out of range. */
 
+/* Dispatch test hooks (read once per process; defaults are the shipped
+ * behaviour, the hooks exist so tests can reach every kernel instantiation):
+ *   RNT_LAT_UNITS=k      N <= 2^10 jobs of <= k (poly, limb) units use the
+ *                        latency engine k_lat (default 512; 0 = never);
+ *   RNT_CLUSTER_UNITS=k  jobs of <= k units use the single-launch cluster
+ *                        kernels (default 2; 0 = never);
+ *   RNT_LAZY=0           keep the [0, 4q) kernels even when every q < 2^60;
+ *   RNT_KS_UNFUSED=1     key switching always takes the unfused path;
+ *   RNT_DEBUG=1          input range validation (above). */
+
 #define RNT_MIN_LOG2N 4u
 #define RNT_MAX_LOG2N 16u
 #define RNT_MAX_LIMBS 1024u
@@ -181,6 +191,23 @@ rnt_status rnt_keyswitch_destroy(rnt_keyswitch ks);
 rnt_status rnt_keyswitch_query(rnt_keyswitch ks, uint32_t* alpha, uint64_t* workspace_bytes);
 rnt_status rnt_keyswitch_apply(rnt_keyswitch ks, uint64_t* out, const uint64_t* d, const uint64_t* evk,
                                const uint64_t* add0, void* stream);
+
+/* HRF-MatVec, the homomorphic-rotation-free matrix-vector product of repack
+ * (tab:repack P:393-395: 0 rotations, n_slot scalar
+ * multiplications over n_slot precomputed rotation ciphertexts).  In the NTT
+ * domain, for every component c < 2, limb l and slot k (reading H1):
+ *   out[c][l][k] = add[c][l][k] + sum_{j < n_slot} pt[j][l][k] * ct[j][c][l][k]  mod q_l
+ * pt:  device [n_slot][n_limbs][N], plaintext diagonals (giant-step automorph
+ *      already applied), NTT form, canonical;
+ * ct:  device [n_slot][2][n_limbs][N], rotation ciphertexts, NTT form, canonical;
+ * add: device [2][n_limbs][N] (the "+ b" of As + b) or NULL (= 0); may equal
+ *      out (accumulate in place);
+ * out: device [2][n_limbs][N], canonical; must not overlap pt or ct.
+ * All pointers 16-byte aligned.  n_slot == 0 writes add (or zeros).  Argument
+ * errors (null / unaligned pointers, overlap, size overflow) return
+ * RNT_E_INVALID_ARG before any launch.  One launch, asynchronous on `stream`. */
+rnt_status rnt_hrf_matvec(rnt_plan p, uint64_t* out, const uint64_t* pt, const uint64_t* ct, uint32_t n_slot,
+                          const uint64_t* add, void* stream);
 
 /* Operation codes for rnt_execute_host. */
 typedef enum {

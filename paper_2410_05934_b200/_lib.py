@@ -29,6 +29,7 @@ SIGNATURES = {
     "rnt_polymul": (_i32, [_vp, _vp, _vp, _vp, _u32, _i32, _i32, _vp]),
     "rnt_automorph": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _vp]),
     "rnt_external_product": (_i32, [_vp, _vp, _vp, _vp, _u32, _u32, _u32, _vp]),
+    "rnt_hrf_matvec": (_i32, [_vp, _vp, _vp, _vp, _u32, _vp, _vp]),
     "rnt_bconv_create": (_i32, [ctypes.POINTER(_vp), _vp, _vp]),
     "rnt_bconv_destroy": (_i32, [_vp]),
     "rnt_bconv_apply": (_i32, [_vp, _vp, _vp, _u32, _vp]),

@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "librnsntt.so")
 SOURCES = ["api.cu", "plan.cpp"]
-HEADERS = ["modarith.cuh", "ntt_small.cuh", "ntt_large.cuh", "keyswitch.cuh", "ntt_cluster.cuh", "ntt_clat.cuh", "plan.h"]
+HEADERS = ["modarith.cuh", "ntt_small.cuh", "ntt_large.cuh", "keyswitch.cuh", "ntt_cluster.cuh", "ntt_clat.cuh", "hrf.cuh", "plan.h"]
 
 NVCC_FLAGS = [
     "-O3",

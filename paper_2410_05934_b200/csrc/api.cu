@@ -21,6 +21,7 @@
 #include "keyswitch.cuh"
 #include "ntt_cluster.cuh"
 #include "ntt_clat.cuh"
+#include "hrf.cuh"
 #include "plan.h"
 
 using namespace rnt;
@@ -247,75 +248,29 @@ static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, co
   return RNT_OK;
 }
 
-// Tuning knob (benchmarks only): RNT_SMALL_VARIANT selects the N=2^10 launch
-// configuration; 0 (default) = 4 warps/CTA, no CTA barrier.
-static int small_variant() {
-  static const int v = env_int("RNT_SMALL_VARIANT", 0);
-  return v;
-}
-
+// Dispatch test hook (documented in rnsntt.h): RNT_LAZY=0 keeps the [0, 4q)
+// kernels even when every modulus is below 2^60.
 static bool lazy_enabled() {
   static const bool v = env_int("RNT_LAZY", 1) != 0;
   return v;
 }
 
-template <int LOGN, int MODE, int W>
-static rnt_status launch_warp_tma(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
-                                  uint32_t batch, cudaStream_t st) {
-  static std::atomic<uint64_t> attr{0};
-  const size_t smem = warp_tma_smem_bytes<W>();
-  if (rnt_status s = ensure_attr(k_warp_tma<LOGN, MODE, W>, smem, attr); s != RNT_OK) return s;
-  int max_ctas_per_sm = 0;
-  RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_ctas_per_sm, k_warp_tma<LOGN, MODE, W>, W * 32, smem));
-  if (max_ctas_per_sm < 1) max_ctas_per_sm = 1;
-  // persistent grid: as many warps as fit, then shrink so every warp runs the
-  // same number of iterations (no tail imbalance).
-  const uint64_t groups = ((uint64_t)batch + WarpCfg<LOGN>::P - 1) / WarpCfg<LOGN>::P;
-  for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
-    const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
-    uint64_t max_warps = (uint64_t)num_sms() * max_ctas_per_sm * W / nl;
-    if (max_warps < W) max_warps = W;
-    const uint64_t iters = (groups + max_warps - 1) / max_warps;
-    const uint64_t warps = (groups + iters - 1) / iters;
-    dim3 grid((unsigned)((warps + W - 1) / W), nl);
-    k_warp_tma<LOGN, MODE, W><<<grid, W * 32, smem, st>>>(
-        out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
-        p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
-    rnt_status s = after_launch();
-    if (s != RNT_OK) return s;
-  }
-  return RNT_OK;
-}
+// CTAs per SM the warp engine is compiled for (2 warps each); experiments rebuild
+// with RNT_NVCC_EXTRA=-DRNT_WARP_MINB=n (build.py), the shipped value is 12.
+#ifndef RNT_WARP_MINB
+#define RNT_WARP_MINB 12
+#endif
 
 template <int LOGN, int MODE>
 static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                               int bcast, uint32_t batch, cudaStream_t st) {
-  if constexpr (LOGN == 10 && MODE != 3) {
-    switch (small_variant()) {
-      case 5: return launch_warp_tma<LOGN, MODE, 4>(p, out, in, bop, bcast, batch, st);
-      case 6: return launch_warp_tma<LOGN, MODE, 2>(p, out, in, bop, bcast, batch, st);
-      case 1: return launch_warp_v<LOGN, MODE, 4, 4, false>(p, out, in, bop, bcast, batch, st);
-      case 7: return launch_warp_v<LOGN, MODE, kTeamWarps, 1, false>(p, out, in, bop, bcast, batch, st);
-      case 8: return launch_warp_v<LOGN, MODE, 2, 8, false, 4>(p, out, in, bop, bcast, batch, st);
-      case 9: return launch_warp_v<LOGN, MODE, 4, 4, false, 3>(p, out, in, bop, bcast, batch, st);
-      case 10: return launch_warp_v<LOGN, MODE, 2, 8, false, 5>(p, out, in, bop, bcast, batch, st);
-      case 11: return launch_warp_v<LOGN, MODE, 2, 16, false, 3>(p, out, in, bop, bcast, batch, st);
-      case 12: return launch_warp_v<LOGN, MODE, 4, 6, false, 3>(p, out, in, bop, bcast, batch, st);
-      case 13: return launch_warp_v<LOGN, MODE, 2, 16, false, 2>(p, out, in, bop, bcast, batch, st);
-      case 14: return launch_warp_v<LOGN, MODE, 1, 24, false, 3>(p, out, in, bop, bcast, batch, st);
-      case 16:   // LZ with the plain radix-8 schedule 3 + 3 + 3 + 1 (the default before the split tail)
-        if (p->lazy60) return launch_warp_v<LOGN, MODE, 2, 12, false, 3, true>(p, out, in, bop, bcast, batch, st);
-        break;
-      default: break;
-    }
-  }
-  // default: radix-8 passes (N=2^10: 3+3+3+1), 2 warps per CTA, <= 85 registers
-  // (24 warps/SM) -- fastest measured (profiles/r01/README.md); lazy CT ranges
-  // when every modulus is below 2^60 (env RNT_LAZY=0 disables)
-  // LZ kernels use the split-tail schedule (N = 2^10: 3 + 3 + 2 + 2; cfg5 k_warp 0.2643 -> 0.2623
-  // ms, cfg2 0.0847 -> 0.0813 ms): the polymul turn pass works on 4-coefficient groups
-  if (p->lazy60 && lazy_enabled()) return launch_warp_v<LOGN, MODE, 2, 12, false, 32, true>(p, out, in, bop, bcast, batch, st);
-  return launch_warp_v<LOGN, MODE, 2, 12, false, 3>(p, out, in, bop, bcast, batch, st);
+  // radix-8 passes, 2 warps per CTA, <= 85 registers (24 warps/SM) -- fastest measured
+  // (profiles/r01/README.md); lazy CT ranges with the split-tail schedule (N = 2^10:
+  // 3 + 3 + 2 + 2, the polymul turn pass on 4-coefficient groups) when every modulus is
+  // below 2^60; [0, 4q) Harvey ranges with 3 + 3 + 3 + 1 otherwise
+  if (p->lazy60 && lazy_enabled())
+    return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true>(p, out, in, bop, bcast, batch, st);
+  return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 
 // Latency engine (k_lat, ntt_small.cuh) for jobs of at most lat_units()
@@ -382,19 +337,11 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // CTA order for the two-pass kernels: block b -> (sub-block, poly, limb) with
 // the sub-block fastest, then the polynomial, then the limb, so CTAs that
 // share a limb's twiddle rows run back to back (L2 reuse across the batch).
-// Large-N launch variant bits (env RNT_LARGE_VARIANT): 1 = 8-column pass-1
-// tiles, 2 = RPC/4 row CTAs, 4 = warp-engine rows (k_rows).  Unset: 5 for
-// N = 2^16 jobs of >= 192 limb-units (cfg4 0.827 -> 0.804 ms), else 0 (k_rows
+// Launch shape chosen per call by large_op: N = 2^16 jobs of >= 192 limb-units
+// (cfg4) take 8-column pass-1 tiles and the warp-engine rows (k_rows; cfg4
+// 0.827 -> 0.804 ms); smaller jobs the 16-column tiles and k_row (k_rows
 // under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
-static int large_variant_env() {
-  static const int v = env_int("RNT_LARGE_VARIANT", -1);
-  return v;
-}
-static thread_local int g_large_auto = 0;   // set by large_op for the current call
-static int large_variant() {
-  const int v = large_variant_env();
-  return v >= 0 ? v : g_large_auto;
-}
+static thread_local bool g_large_wide = false;   // set by large_op for the current call
 
 template <int LOGN, int CT, bool LZ = false>
 static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
@@ -420,10 +367,10 @@ static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64*
   // forward columns with lazy CT ranges when the plan allows it; the row pass
   // that consumes them (launch_row) makes the same choice
   if (!inv && p->lazy60 && lazy_enabled()) {
-    if (large_variant() & 1) return launch_col_v<LOGN, 8, true>(p, inv, after_mont, out, in, batch, st);
+    if (g_large_wide) return launch_col_v<LOGN, 8, true>(p, inv, after_mont, out, in, batch, st);
     return launch_col_v<LOGN, kColTile, true>(p, inv, after_mont, out, in, batch, st);
   }
-  if (large_variant() & 1) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
+  if (g_large_wide) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
   return launch_col_v<LOGN, kColTile>(p, inv, after_mont, out, in, batch, st);
 }
 
@@ -465,17 +412,14 @@ static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in,
 template <int LOGN, int MODE>
 static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                              uint32_t batch, cudaStream_t st) {
-  constexpr int R4 = TwoPass<LOGN>::RPC / 4 > 0 ? TwoPass<LOGN>::RPC / 4 : 1;
   if constexpr (MODE != 1) {
     // input from an LZ forward column pass (launch_col makes the same choice)
     if (p->lazy60 && lazy_enabled()) {
-      if (large_variant() & 4) return launch_rows_warp<LOGN, MODE, true>(p, out, in, bop, bcast, batch, st);
-      if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4, true>(p, out, in, bop, bcast, batch, st);
+      if (g_large_wide) return launch_rows_warp<LOGN, MODE, true>(p, out, in, bop, bcast, batch, st);
       return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC, true>(p, out, in, bop, bcast, batch, st);
     }
   }
-  if (large_variant() & 4) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
-  if (large_variant() & 2) return launch_row_v<LOGN, MODE, R4>(p, out, in, bop, bcast, batch, st);
+  if (g_large_wide) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
@@ -483,7 +427,7 @@ template <int LOGN>
 static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
-  g_large_auto = (LOGN == 16 && (uint64_t)batch * p->L >= 192) ? 5 : 0;
+  g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= 192;
   switch (op) {
     case 0:  // forward
       if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
@@ -501,7 +445,7 @@ static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in,
 
 // Single-launch cluster path (ntt_cluster.cuh) for latency-bound jobs: a
 // cluster of C CTAs owns one limb on chip.  Used when batch * L is at most
-// cluster_units() (env RNT_CLUSTER_UNITS; 0 disables).
+// cluster_units() (dispatch test hook RNT_CLUSTER_UNITS; 0 disables).
 static int cluster_units() {
   static const int v = env_int("RNT_CLUSTER_UNITS", 2);
   return v;
@@ -547,8 +491,7 @@ static rnt_status cluster_op_c(const rnt_plan_s* p, int op, u64* out, const u64*
 }
 
 // Latency cluster kernel (ntt_clat.cuh): E = 4 coefficients per thread and C CTAs
-// per limb (defaults in clat_op; env RNT_CLAT_C = 8 / 16 overrides where the
-// geometry is valid); env RNT_CLAT=0 falls back to k_cluster.
+// per limb (clat_op).
 template <int LOGN, int C, int E, int MODE>
 static rnt_status launch_clat_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                 uint32_t batch, cudaStream_t st) {
@@ -601,19 +544,11 @@ template <int LOGN>
 static rnt_status clat_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                           uint32_t batch, cudaStream_t st) {
   constexpr int DC = LOGN <= 12 ? 8 : 16, DE = 4;
-  static const int c = env_int("RNT_CLAT_C", DC) == 8 ? 8 : 16;
-  if (c != DC) {
-    if (c == 8) { if constexpr (clat_valid<LOGN, 8, DE>()) return clat_op_ce<LOGN, 8, DE>(p, op, out, in, bop, bcast, batch, st); }
-    else { if constexpr (clat_valid<LOGN, 16, DE>()) return clat_op_ce<LOGN, 16, DE>(p, op, out, in, bop, bcast, batch, st); }
-  }
   static_assert(clat_valid<LOGN, DC, DE>(), "default latency geometry");
   return clat_op_ce<LOGN, DC, DE>(p, op, out, in, bop, bcast, batch, st);
 }
 
-static bool clat_enabled() {
-  static const bool v = env_int("RNT_CLAT", 1) != 0;
-  return v;
-}
+static bool clat_enabled() { return true; }
 
 template <int LOGN>
 static rnt_status cluster_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
@@ -623,14 +558,9 @@ static rnt_status cluster_op(const rnt_plan_s* p, int op, u64* out, const u64* i
   if constexpr (LOGN <= 15) {
     if (clat_enabled()) return clat_op<LOGN>(p, op, out, in, bop, bcast, batch, st);
   }
-  // cluster size: 8 CTAs up to 2^14, 16 above (measured, single-polynomial
-  // latency); env RNT_CLUSTER_C = 8 or 16 forces one
-  static const int csz = [] {
-    const int v = env_int("RNT_CLUSTER_C", 0);
-    return v == 0 ? 0 : (v == 8 ? 8 : 16);
-  }();
-  if (csz == 8 || (csz == 0 && LOGN <= 14)) return cluster_op_c<LOGN, 8>(p, op, out, in, bop, bcast, batch, st);
-  return cluster_op_c<LOGN, 16>(p, op, out, in, bop, bcast, batch, st);
+  // cluster size: 8 CTAs up to 2^14, 16 above (measured, single-polynomial latency)
+  if constexpr (LOGN <= 14) return cluster_op_c<LOGN, 8>(p, op, out, in, bop, bcast, batch, st);
+  else return cluster_op_c<LOGN, 16>(p, op, out, in, bop, bcast, batch, st);
 }
 
 static rnt_status cluster_dispatch(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
@@ -717,10 +647,6 @@ struct rnt_bconv_s {
   TW* d_qhat_p = nullptr;   // [K][L]: Shoup pair of (Q/q_i mod p_j) w.r.t. p_j
 };
 
-// The CTA-parallel kernel (one warp per decomposed polynomial) is the default
-// (N = 2^10, l = 3: 1024 / 4096 / 16384 slots 0.127 / 0.411 / 1.55 ms vs 0.209 /
-// 0.537 / 1.73 ms for the single-warp k_extprod); env RNT_EXTPROD=0 selects k_extprod.
-
 template <int LOGN, int LV, int KM, bool LZ>
 static rnt_status launch_extprod_cta_v(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                        DigitSpec ds, cudaStream_t st) {
@@ -742,11 +668,13 @@ static rnt_status launch_extprod_cta(const rnt_plan_s* p, u64* out, const u64* c
   return launch_extprod_cta_v<LOGN, LV, 3, false>(p, out, c, z, n_slot, ds, st);
 }
 
+// N = 2^10 (the TFHE size): the CTA-parallel kernel, one warp per decomposed
+// polynomial (l = 3: 1024 / 4096 / 16384 slots 0.127 / 0.411 / 1.55 ms vs 0.209 /
+// 0.537 / 1.73 ms for the single-warp kernel); smaller N: the single-warp k_extprod.
 template <int LOGN>
 static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, const u64* z, uint32_t n_slot,
                                  DigitSpec ds, cudaStream_t st) {
-  static const bool cta = env_int("RNT_EXTPROD", 1) != 0;
-  if constexpr (LOGN == 10) if (cta) {
+  if constexpr (LOGN == 10) {
     switch (ds.levels) {
       case 1: return launch_extprod_cta<LOGN, 1>(p, out, c, z, n_slot, ds, st);
       case 2: return launch_extprod_cta<LOGN, 2>(p, out, c, z, n_slot, ds, st);
@@ -756,16 +684,17 @@ static rnt_status launch_extprod(const rnt_plan_s* p, u64* out, const u64* c, co
       case 6: return launch_extprod_cta<LOGN, 6>(p, out, c, z, n_slot, ds, st);
       case 7: return launch_extprod_cta<LOGN, 7>(p, out, c, z, n_slot, ds, st);
       case 8: return launch_extprod_cta<LOGN, 8>(p, out, c, z, n_slot, ds, st);
-      default: break;
+      default: return RNT_E_INVALID_ARG;
     }
+  } else {
+    static std::atomic<uint64_t> attr{0};
+    const size_t smem = (size_t)2 * kWarpBuf * 8;
+    if (rnt_status s = ensure_attr(k_extprod<LOGN>, smem, attr); s != RNT_OK) return s;
+    const uint64_t per_cta = 2ull * (kWarpElems >> LOGN);
+    const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
+    k_extprod<LOGN><<<(unsigned)grid, 64, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc, n_slot, ds);
+    return after_launch();
   }
-  static std::atomic<uint64_t> attr{0};
-  const size_t smem = (size_t)2 * kWarpBuf * 8;
-  if (rnt_status s = ensure_attr(k_extprod<LOGN>, smem, attr); s != RNT_OK) return s;
-  const uint64_t per_cta = 2ull * (kWarpElems >> LOGN);
-  const uint64_t grid = (n_slot + per_cta - 1) / per_cta;
-  k_extprod<LOGN><<<(unsigned)grid, 64, smem, st>>>(out, c, z, p->d_fwd, p->d_inv, p->d_lc, n_slot, ds);
-  return after_launch();
 }
 
 // BConv tables from basis {q_i} (L) to {p_j} (K) (reading G3):
@@ -801,14 +730,8 @@ static void bconv_tables(const uint64_t* q, uint32_t L, const uint64_t* p, uint3
 // column pass with the lift on load (k_col_fwd<.., MODUP>), then the row pass
 // with the key multiply-accumulate (k_row_mac).  E: [dnum][LK][N] scratch.
 // Digit split of the fused key product (k_row_mac blockIdx.z): dnum digits in
-// `split` partial sums, added by k_ks_sum.  Env RNT_KS_SPLIT overrides.
-static uint32_t ks_split(uint32_t dnum) {
-  static const int v = [] {
-    const int e = env_int("RNT_KS_SPLIT", 1);
-    return e < 1 ? 1 : (e > 8 ? 8 : e);
-  }();
-  return (uint32_t)v < dnum ? (uint32_t)v : dnum;
-}
+// `split` partial sums, added by k_ks_sum (2..5 measured no faster: 1).
+static uint32_t ks_split(uint32_t dnum) { return dnum ? 1u : 0u; }
 
 template <int LOGN, bool LZ>
 static rnt_status ks_fused_launch_v(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk,
@@ -1065,12 +988,14 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   // A single polynomial with many limbs (cfg3) launches few CTAs per kernel and
   // pays each kernel's ramp and tail three times; running G limb windows as
   // independent kernel chains on G streams lets the windows overlap
-  // (measured: 2^16 x 45 limbs polymul 0.103 -> 0.094 ms with G = 2).
-  static const int split_g = [] {
-    const int v = env_int("RNT_SPLIT", 2);
-    return v > 4 ? 4 : v;
-  }();
-  if (split_g > 1 && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
+  // (measured: 2^16 x 45 limbs polymul 0.103 -> 0.094 ms with G = 2; 3 and 4 no
+  // better).  The window streams belong to the plan, so concurrent callers of one
+  // plan serialise on them; a stream under CUDA-graph capture skips the split (the
+  // plan's streams must not join another thread's capture).
+  constexpr int split_g = 2;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  RNT_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
     std::lock_guard<std::mutex> g(p->split_mu);
     for (int i = 0; i < split_g; ++i)
       if (!p->split[i]) RNT_CUDA(cudaStreamCreateWithFlags(&p->split[i], cudaStreamNonBlocking));
@@ -1153,6 +1078,50 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
   k_automorph<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in), p->d_lc, p->L, p->logn, galois_elt, ginv,
       ntt_domain ? 1 : 0, total);
+  return after_launch();
+}
+
+// HRF-MatVec (f4): one launch of k_hrf_matvec (hrf.cuh), a grid-stride loop
+// over the L N / 2 slot pairs, enough CTAs for every SM.  Experiments rebuild with
+// RNT_NVCC_EXTRA=-DRNT_HRF_UNROLL=n / -DRNT_HRF_CTAS_PER_SM=n (build.py).
+#ifndef RNT_HRF_UNROLL
+#define RNT_HRF_UNROLL 4
+#endif
+#ifndef RNT_HRF_CTAS_PER_SM
+#define RNT_HRF_CTAS_PER_SM 8
+#endif
+rnt_status rnt_hrf_matvec(rnt_plan p, uint64_t* out, const uint64_t* pt, const uint64_t* ct, uint32_t n_slot,
+                          const uint64_t* add, void* stream) {
+  if (!p || !out || !aligned16(out) || (add && !aligned16(add))) return RNT_E_INVALID_ARG;
+  const uint64_t ln = (uint64_t)p->L << p->logn;
+  if (n_slot) {
+    if (!pt || !ct || !aligned16(pt) || !aligned16(ct)) return RNT_E_INVALID_ARG;
+    const unsigned __int128 bytes = (unsigned __int128)n_slot * 3u * ln * 8u;
+    if (bytes >> 62) return RNT_E_INVALID_ARG;
+    auto overlap = [](const void* a, uint64_t na, const void* b, uint64_t nb) {
+      const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+      return x < y + nb && y < x + na;
+    };
+    const uint64_t ob = 2 * ln * 8;
+    if (overlap(out, ob, pt, (uint64_t)n_slot * ln * 8) || overlap(out, ob, ct, (uint64_t)n_slot * 2 * ln * 8))
+      return RNT_E_INVALID_ARG;
+  }
+  rnt_status s = check_plan_device(p);
+  if (s != RNT_OK) return s;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (n_slot) {
+    if ((s = debug_validate(p, pt, n_slot, st)) != RNT_OK) return s;
+    if ((s = debug_validate(p, ct, 2ull * n_slot, st)) != RNT_OK) return s;
+  }
+  if (add && (s = debug_validate(p, add, 2, st)) != RNT_OK) return s;
+  const uint64_t nvec = ln / 2;
+  const int threads = 256;
+  uint64_t blocks = (nvec + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * RNT_HRF_CTAS_PER_SM;
+  if (blocks > cap) blocks = cap;
+  k_hrf_matvec<RNT_HRF_UNROLL><<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(pt),
+                                                        reinterpret_cast<const u64*>(ct), reinterpret_cast<const u64*>(add),
+                                                        p->d_lc, n_slot, p->L, p->logn, nvec);
   return after_launch();
 }
 
@@ -1298,7 +1267,7 @@ rnt_status rnt_keyswitch_create(rnt_keyswitch* out, rnt_plan q_plan, rnt_plan qp
     uint64_t qmax = 0, mmin = ~0ull;
     for (uint32_t i = 0; i < L; ++i) qmax = m[i] > qmax ? m[i] : qmax;
     for (uint32_t t = 0; t < LK; ++t) mmin = m[t] < mmin ? m[t] : mmin;
-    static const bool force_unfused = env_int("RNT_KS_UNFUSED", 0) > 0;
+    static const bool force_unfused = env_int("RNT_KS_UNFUSED", 0) > 0;   // dispatch test hook
     ks->fused = !force_unfused && ks->logn >= 11 && alpha == 1 && qmax / 2 < mmin;
     ks->split = ks->fused ? ks_split(dnum) : 1;
   }
@@ -1463,12 +1432,12 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   // Chunking: chunks over polynomials (batch > 1) or limbs (batch == 1),
   // round-robin over three internal streams so H2D copy, kernels and D2H copy
   // of successive chunks overlap.  Fork/join with the caller's stream by events.
-  // chunk bytes (tuning knob RNT_CHUNK_MB, default 16 MiB, measured best)
-  static const size_t target = (size_t)(env_int("RNT_CHUNK_MB", 16) > 0 ? env_int("RNT_CHUNK_MB", 16) : 16) << 20;
+  // chunk bytes: 16 MiB (measured best of 4 .. 64)
+  constexpr size_t target = (size_t)16 << 20;
   // Granule = one polynomial (batch > 1) or one limb (batch == 1).  Chunks of
   // `target` bytes, except that the first and last chunks ramp (target/8,
-  // /4, /2, ...) so the copy engines start and drain sooner (env RNT_CHUNK_RAMP=0: uniform).
-  static const bool ramp = env_int("RNT_CHUNK_RAMP", 1) > 0;
+  // /4, /2, ...) so the copy engines start and drain sooner (measured better than uniform).
+  constexpr bool ramp = true;
   const size_t gbytes = batch > 1 ? (size_t)p->L * unit_bytes : unit_bytes;
   const size_t G = batch > 1 ? batch : p->L;
   size_t T = target / gbytes;

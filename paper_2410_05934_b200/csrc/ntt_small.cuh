@@ -155,7 +155,6 @@ struct GView {
 // Source kinds of a pass.
 constexpr int kFromBuf = 0;     // padded warp buffer
 constexpr int kFromGlobal = 1;  // global memory (GView)
-constexpr int kFromRaw = 2;     // unpadded shared staging buffer filled by a TMA bulk copy
 
 // Destination kinds of a pass.
 constexpr int kToBuf = 0;      // lazy values back into the warp buffer
@@ -167,8 +166,7 @@ constexpr int kToBufCanon = 2; // canonical values into the warp buffer
 // share T; 2^{n2}: row r + p of a 2^16 limb uses row table r + p).
 // S0: global index of local stage 0 (rows of a 2^16 limb: n1), for the LZ schedule.
 template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false, int S0 = 0>
-__device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2,
-                                         const u64* raw = nullptr) {
+__device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
 #pragma unroll 1
@@ -182,9 +180,6 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
       const u64* s = src.at(g.poly) + jj0;
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
-    } else if constexpr (SRC == kFromRaw) {
-#pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = raw[g.base + i * Geo::LO];
     } else {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
@@ -208,7 +203,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST, int TWS = 0, bool MIRROR = false,
           bool LZT = false>
 __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
-                                         u64 q, u64 q2, const u64* raw = nullptr) {
+                                         u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
 #pragma unroll 1
@@ -222,9 +217,6 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
       const u64* s = src.at(g.poly) + jj0;
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
-    } else if constexpr (SRC == kFromRaw) {
-#pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = raw[g.base + i * Geo::LO];
     } else {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
@@ -246,12 +238,11 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
 
 // Fused turn-around pass of the polymul: last CT pass -> (.) b_hat -> first
 // GS pass, all in registers.  b_hat comes from global memory (bview) or from
-// a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf), or a TMA-staged raw buffer (kFromRaw).
+// a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf).
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC, bool SCALE = true, int TWS = 0,
           bool MIRROR = false, bool LZ = false, int S0 = 0>
 __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
-                                          const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv,
-                                          const u64* raw = nullptr, const u64* braw = nullptr) {
+                                          const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
 #pragma unroll 1
@@ -265,9 +256,6 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
       const u64* s = src.at(g.poly) + jj0;
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = live ? s[i * Geo::LO] : 0ull;
-    } else if constexpr (SRC == kFromRaw) {
-#pragma unroll
-      for (int i = 0; i < (1 << K); ++i) x[i] = raw[g.base + i * Geo::LO];
     } else {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) x[i] = buf[pb + pad_off<LOGN, S, Geo::LO>(i)];
@@ -277,9 +265,6 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
     if constexpr (BSRC == kFromBuf) {
 #pragma unroll
       for (int i = 0; i < (1 << K); ++i) bv[i] = bbuf[pb + pad_off<LOGN, S, Geo::LO>(i)];
-    } else if constexpr (BSRC == kFromRaw) {
-#pragma unroll
-      for (int i = 0; i < (1 << K); ++i) bv[i] = braw[g.base + i * Geo::LO];
     } else {
       const bool live = bview.live(g.poly);
       const u64* b = bview.at(g.poly) + jj0;
@@ -425,139 +410,6 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
                                                                          Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     }
   }
-}
-
-
-// ---- TMA-staged persistent variant ---------------------------------------------
-// Each warp loops over its limb's polynomial groups.  Inputs are staged by a
-// 1-D TMA bulk copy (cp.async.bulk, completion on a per-warp mbarrier) into an
-// unpadded raw buffer that the first pass reads; the copy for the next
-// operand is issued as soon as the raw buffer is consumed, so global-memory
-// latency overlaps the butterfly passes (SASS: UBLKCP + SYNCS).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-
-// Stage the P polynomials of view v starting at group `grp` into raw (lane 0).
-template <int LOGN>
-__device__ __forceinline__ void stage(u64* raw, const GView& v, uint64_t p0, uint64_t* bar) {
-  constexpr int N = 1 << LOGN;
-  constexpr int P = WarpCfg<LOGN>::P;
-  uint32_t n = 0;
-#pragma unroll
-  for (int p = 0; p < P; ++p) n += (p0 + p < v.units) ? 1u : 0u;
-  mbar_expect_tx(bar, n * N * 8u);
-#pragma unroll
-  for (int p = 0; p < P; ++p)
-    if (p0 + p < v.units) bulk_g2s(raw + p * N, v.base + (p0 + p) * v.stride, N * 8u, bar);
-}
-
-// MODE 0: forward, 1: inverse, 2: polymul with NTT-form b.  grid = (X, L).
-template <int LOGN, int MODE, int W>
-__global__ void __launch_bounds__(W * 32)
-k_warp_tma(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
-           const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc, uint32_t L,
-           uint32_t B) {
-  using C = WarpCfg<LOGN>;
-  constexpr int N = C::N;
-  extern __shared__ __align__(16) u64 smem[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t l = blockIdx.y;
-  u64* raw = smem + (size_t)warp * (kWarpElems + kWarpBuf + 2);
-  u64* buf = raw + kWarpElems;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(buf + kWarpBuf);
-  const uint64_t ngroups = ((uint64_t)B + C::P - 1) / C::P;
-  const uint64_t stride_w = (uint64_t)gridDim.x * W;
-  uint64_t grp = (uint64_t)blockIdx.x * W + warp;
-  if (grp >= ngroups) return;
-  const u64 q = lc[l].q, q2 = lc[l].q2;
-  const uint64_t stride = (uint64_t)L * N;
-  const GView src{in + (uint64_t)l * N, 0, stride, B};
-  const GView bsrcv{bop ? bop + (uint64_t)l * N : nullptr, 0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
-  const TW* Tf = tw_fwd + (size_t)l * N;
-  const TW* Ti = tw_inv + (size_t)l * N;
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  uint32_t phase = 0;
-  if (lane == 0) stage<LOGN>(raw, src, grp * C::P, bar);
-  for (; grp < ngroups; grp += stride_w) {
-    const uint64_t p0 = grp * C::P;
-    const uint64_t nxt = grp + stride_w;
-    const GView dst{out + (uint64_t)l * N, p0, stride, B};
-    const GView gv{src.base, p0, stride, B};
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    if constexpr (MODE == 0) {
-      if constexpr (C::NPASS == 3) {
-        fwd_pass<LOGN, 0, C::K0, kFromRaw, kToBuf>(buf, gv, dst, lane, Tf, q, q2, raw);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0 && nxt < ngroups) stage<LOGN>(raw, src, nxt * C::P, bar);
-        fwd_pass<LOGN, C::K0, C::K1, kFromBuf, kToBuf>(buf, gv, dst, lane, Tf, q, q2);
-        fwd_pass<LOGN, C::K0 + C::K1, C::K2, kFromBuf, kToGlobal>(buf, gv, dst, lane, Tf, q, q2);
-      }
-    } else if constexpr (MODE == 1) {
-      if constexpr (C::NPASS == 3) {
-        inv_pass<LOGN, C::K0 + C::K1, C::K2, kFromRaw, false, false>(buf, gv, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1,
-                                                                    q, q2, raw);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0 && nxt < ngroups) stage<LOGN>(raw, src, nxt * C::P, bar);
-        inv_pass<LOGN, C::K0, C::K1, kFromBuf, false, false>(buf, gv, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
-        inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, gv, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q, q2);
-      }
-    } else {
-      if constexpr (C::NPASS == 3) {
-        const u64 qinv = lc[l].qinv;
-        const TW s0 = lc[l].ninvR, s1 = lc[l].ninvR_w1;
-        fwd_pass<LOGN, 0, C::K0, kFromRaw, kToBuf>(buf, gv, dst, lane, Tf, q, q2, raw);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) stage<LOGN>(raw, GView{bsrcv.base, 0, bsrcv.stride, bsrcv.units}, b_bcast ? 0 : p0, bar);
-        fwd_pass<LOGN, C::K0, C::K1, kFromBuf, kToBuf>(buf, gv, dst, lane, Tf, q, q2);
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        turn_pass<LOGN, C::K0 + C::K1, C::K2, kFromBuf, false, kFromRaw>(buf, gv, dst, bsrcv, nullptr, lane, Tf, Ti,
-                                                                        s0, s1, q, q2, qinv, nullptr, raw);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0 && nxt < ngroups) stage<LOGN>(raw, src, nxt * C::P, bar);
-        inv_pass<LOGN, C::K0, C::K1, kFromBuf, false, false>(buf, gv, dst, lane, Ti, s0, s1, q, q2);
-        inv_pass<LOGN, 0, C::K0, kFromBuf, true, true>(buf, gv, dst, lane, Ti, s0, s1, q, q2);
-      }
-    }
-  }
-}
-
-template <int W>
-inline size_t warp_tma_smem_bytes() {
-  return (size_t)W * (kWarpElems + kWarpBuf + 2) * 8;
 }
 
 

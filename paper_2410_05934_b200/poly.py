@@ -93,6 +93,13 @@ def _same_basis(a: RnsPoly, b: RnsPoly) -> None:
         raise BasisMismatch("operands are in different RNS bases")
 
 
+def _same_shape(a: RnsPoly, o: RnsPoly) -> None:
+    """`out` must hold exactly a's batch (the kernels write batch * L * N words)."""
+    _same_shape(a, o)
+    if o.batch != a.batch:
+        raise ValueError(f"out batch {o.batch} != operand batch {a.batch}")
+
+
 def _plan_for(p: RnsPoly, plan):
     if plan is None:
         return p.plan
@@ -117,7 +124,7 @@ def forward(a: RnsPoly, plan=None, out: RnsPoly | None = None, stream=None) -> R
     _need(a, COEFF, "ntt_forward")
     pl = _plan_for(a, plan)
     o = out if out is not None else a.empty_like(EVAL)
-    _same_basis(a, o)
+    _same_shape(a, o)
     _api()[0](pl, o.data, a.data, stream=stream)
     o.domain = EVAL
     return o
@@ -128,7 +135,7 @@ def inverse(a: RnsPoly, plan=None, out: RnsPoly | None = None, stream=None) -> R
     _need(a, EVAL, "ntt_inverse")
     pl = _plan_for(a, plan)
     o = out if out is not None else a.empty_like(COEFF)
-    _same_basis(a, o)
+    _same_shape(a, o)
     _api()[1](pl, o.data, a.data, stream=stream)
     o.domain = COEFF
     return o
@@ -143,7 +150,7 @@ def pointwise_mul(a: RnsPoly, b: RnsPoly, out: RnsPoly | None = None, stream=Non
     if b.batch not in (1, a.batch):
         raise ValueError(f"batch mismatch: {a.batch} vs {b.batch}")
     o = out if out is not None else a.empty_like(EVAL)
-    _same_basis(a, o)
+    _same_shape(a, o)
     _api()[2](a.plan, o.data, a.data, b.data, batch=a.batch, b_broadcast=(b.batch != a.batch), stream=stream)
     o.domain = EVAL
     return o
@@ -157,7 +164,7 @@ def polymul(a: RnsPoly, b: RnsPoly, out: RnsPoly | None = None, stream=None) -> 
     if b.batch not in (1, a.batch):
         raise ValueError(f"batch mismatch: {a.batch} vs {b.batch}")
     o = out if out is not None else a.empty_like(COEFF)
-    _same_basis(a, o)
+    _same_shape(a, o)
     _api()[3](a.plan, o.data, a.data, b.data, b_is_eval=(b.domain == EVAL), batch=a.batch,
               b_broadcast=(b.batch != a.batch), stream=stream)
     o.domain = COEFF
@@ -169,7 +176,7 @@ def automorph(a: RnsPoly, galois_elt: int, out: RnsPoly | None = None, stream=No
     if galois_elt % 2 == 0:
         raise ValueError("Galois element must be odd")
     o = out if out is not None else a.empty_like()
-    _same_basis(a, o)
+    _same_shape(a, o)
     _api()[4](a.plan, o.data, a.data, galois_elt, ntt_domain=(a.domain == EVAL), batch=a.batch, stream=stream)
     o.domain = a.domain
     return o

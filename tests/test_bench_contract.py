@@ -44,5 +44,8 @@ def test_our_arm_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 4096 * 1024 * 8
     assert d["step_ms"]["min"] <= d["step_ms"]["median"] <= d["step_ms"]["p90"]
     assert "sm_mhz" in d["clocks"]
+    # the timed outputs equal the oracle's (gathered per-unit digests vs tests/golden)
+    assert d["digests_ok"] is True and d["gpus_active"] == 1
+    assert d["digests"]["e2e_outputs_equal_device_outputs"] is True
     # value = limb-transforms per step / step time
     assert abs(d["value"] - 2 * 4096 / (d["ms_per_step"] * 1e-3)) / d["value"] < 1e-6

@@ -2,7 +2,9 @@
 the limb x batch shard planner, shard-local input
 generation from global counters, and digest gathering.  Each rank computes
 its shard with the CPU oracle; rank 0 checks the gathered per-unit digests
-against the unsharded computation.  No GPU needed."""
+against the unsharded computation.  The bench.py launcher itself (`--gpus 2`
+re-launching under torch.distributed.run) and its shard / digest helpers are
+driven here on CPU too.  No GPU needed."""
 import importlib.util
 import os
 import socket
@@ -143,3 +145,85 @@ def test_gloo_world2_sharded_digests_equal_unsharded():
     ok, n, tmax = q.get(timeout=10)
     assert ok and n == sum(p.limbs * p.polys for p in PARTS)
     assert tmax == 2.0
+
+
+def _bench_module():
+    spec = importlib.util.spec_from_file_location("rnt_bench", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    sys.modules["rnt_bench"] = m
+    spec.loader.exec_module(m)
+    return m
+
+
+def _bench_worker(rank, world, port, wl, q):
+    """bench.py's own shard plan / input / digest / gather helpers, the CUDA compute
+    replaced by the oracle (test infrastructure): the gathered hash must equal the
+    golden oracle hash bench.py checks on the GPU (tests/golden/bench_digests.json)."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+
+        B = _bench_module()
+        parts = B.WORKLOADS[wl]["parts"]
+        rows = []
+        for blk in B.plan_blocks(parts, world, rank, "strong"):
+            a, bh = B.block_inputs(blk)
+            psi = [O.min_psi(qq, blk["logn"]) for qq in blk["mods"]]
+            c = O.batch(O.OP_POLYMUL_EVAL, a, blk["mods"], psi, b=bh, n_threads=4)
+            rows += B.block_digests(blk, c)
+        allr = B.gather_rows(rows, world)
+        if rank == 0:
+            q.put((B.check_digests(wl, allr), len(allr), len(rows)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("wl", ["cfg3", "cfg2"])
+def test_gloo_world2_bench_shards_match_golden_digests(wl):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, wl, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(280)
+        assert p.exitcode == 0
+    ok, n, n0 = q.get(timeout=10)
+    assert ok is True
+    assert 0 < n0 < n   # rank 0 owned a strict part of the units
+
+
+def test_bench_relaunch_command():
+    B = _bench_module()
+    cmd = B.relaunch_cmd(8, ["--gpus", "8", "--steps", "3"])
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "127.0.0.1" in cmd
+    assert cmd[-3:] == ["--gpus", "8", "--steps", "3"][-3:] and cmd[-4] == "--gpus"
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_bench_gpus2_launcher_gloo(scaling):
+    """`bench.py --gpus 2` without torchrun env re-launches itself as 2 ranks; the
+    ranks plan their shards, generate their inputs and all-gather digests."""
+    import json
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check",
+                        "--workload", "cfg5", "--scaling", scaling], capture_output=True, text=True, timeout=280,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["digests_match"] is True and d["max_rank"] == 2.0
+    assert d["units"] == (45 + 16384) * (2 if scaling == "weak" else 1)
