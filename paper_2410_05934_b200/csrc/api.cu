@@ -844,7 +844,10 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   RNT_CUDA(cudaSetDevice(device));
 
   rnt_plan_s* p = new (std::nothrow) rnt_plan_s;
-  if (!p) return RNT_E_OOM;
+  if (!p) {
+    cudaSetDevice(prev);   // leave the caller's current device as it was
+    return RNT_E_OOM;
+  }
   p->logn = log2n;
   p->L = n_limbs;
   p->device = device;
@@ -1178,10 +1181,16 @@ rnt_status rnt_bconv_apply(rnt_bconv c, uint64_t* out, const uint64_t* in, uint3
   const size_t smem = (size_t)c->L * kBcTile * 8;
   if (rnt_status s = set_smem(k_bconv, smem); s != RNT_OK) return s;
   const uint32_t n = 1u << c->logn;
-  dim3 grid((n + kBcTile - 1) / kBcTile, batch);
-  k_bconv<<<grid, kBcTile, smem, (cudaStream_t)stream>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in),
-                                                         c->d_src, c->d_dst, c->d_qhat_p, c->L, c->K, c->logn);
-  return after_launch();
+  // grid.y carries the polynomial: chunks of at most 65535 polynomials per launch
+  for (uint32_t b0 = 0; b0 < batch; b0 += 65535u) {
+    const uint32_t nb = batch - b0 < 65535u ? batch - b0 : 65535u;
+    dim3 grid((n + kBcTile - 1) / kBcTile, nb);
+    k_bconv<<<grid, kBcTile, smem, (cudaStream_t)stream>>>(
+        reinterpret_cast<u64*>(out) + (size_t)b0 * c->K * n, reinterpret_cast<const u64*>(in) + (size_t)b0 * c->L * n,
+        c->d_src, c->d_dst, c->d_qhat_p, c->L, c->K, c->logn);
+    if (rnt_status st = after_launch(); st != RNT_OK) return st;
+  }
+  return RNT_OK;
 }
 
 rnt_status rnt_keyswitch_destroy(rnt_keyswitch ks) {

@@ -568,6 +568,20 @@ def test_bconv(logn, L, K, batch):
         assert np.array_equal(got[b], O.bconv(x[b], src, dst))
 
 
+def test_bconv_batch_above_grid_limit():
+    """batch > 65535 polynomials: the launch is chunked over grid.y."""
+    logn, L, K, batch = 4, 2, 1, 70001
+    qs = O.primes(logn, L + K)
+    src, dst = qs[:L], qs[L:]
+    bc = R.BConv(R.Plan(logn, src), R.Plan(logn, dst))
+    x = inputs.residues(43, batch, src, 1 << logn)
+    out = empty_dev((batch, K, 1 << logn))
+    bc(out, to_dev(x))
+    got = from_dev(out)
+    for b in list(range(0, 40)) + list(range(65500, 65600)) + list(range(batch - 40, batch)):
+        assert np.array_equal(got[b], O.bconv(x[b], src, dst))
+
+
 def test_modup_pipeline_intt_bconv_ntt():
     """CKKS ModUp: NTT-form limbs over Q -> INTT -> BConv -> NTT over P,
     composed from the library calls, against the oracle composition."""
