@@ -228,18 +228,19 @@ static rnt_status set_smem(K kern, size_t smem) {
 }
 
 // ---------------------------------------------------------------- launchers
-template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false>
+template <int LOGN, int MODE, int W, int MINB, bool SYNC, int KM = 4, bool LZ = false, int TEAM = 1>
 static rnt_status launch_warp_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                                 int bcast, uint32_t batch, cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
-  const size_t smem = warp_smem_bytes<LOGN, MODE, W>();
-  if (rnt_status s = ensure_attr(k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ>, smem, attr); s != RNT_OK) return s;
-  const uint64_t per_cta = (uint64_t)W * WarpCfg<LOGN>::P;
+  auto kern = k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ, TEAM>;
+  const size_t smem = warp_smem_bytes<LOGN, MODE, W, TEAM>();
+  if (rnt_status s = ensure_attr(kern, smem, attr); s != RNT_OK) return s;
+  const uint64_t per_cta = (uint64_t)(W / TEAM) * WarpCfg<LOGN>::P;
   const uint64_t gx = (batch + per_cta - 1) / per_cta;
   for (uint32_t l0 = 0; l0 < p->L; l0 += 65535u) {
     const uint32_t nl = p->L - l0 < 65535u ? p->L - l0 : 65535u;
     dim3 grid((unsigned)gx, nl);
-    k_warp<LOGN, MODE, W, MINB, SYNC, KM, LZ><<<grid, W * 32, smem, st>>>(
+    kern<<<grid, W * 32, smem, st>>>(
         out + ((size_t)l0 << LOGN), in + ((size_t)l0 << LOGN), bop ? bop + ((size_t)l0 << LOGN) : nullptr, bcast,
         p->d_fwd + ((size_t)l0 << LOGN), p->d_inv + ((size_t)l0 << LOGN), p->d_lc + l0, p->L, batch);
     rnt_status s = after_launch();
@@ -260,6 +261,15 @@ static bool lazy_enabled() {
 #ifndef RNT_WARP_MINB
 #define RNT_WARP_MINB 12
 #endif
+// Team size by batch (N = 2^10 polymul units): a CTA of TEAM warps per polynomial
+// when the job fills fewer than RNT_TEAM{2,4}_WAVES waves of one-warp units
+// (experiments: -DRNT_TEAM2_WAVES=x / -DRNT_TEAM4_WAVES=x; 0 disables).
+#ifndef RNT_TEAM2_WAVES
+#define RNT_TEAM2_WAVES 0
+#endif
+#ifndef RNT_TEAM4_WAVES
+#define RNT_TEAM4_WAVES 0
+#endif
 
 template <int LOGN, int MODE>
 static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
@@ -268,8 +278,16 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   // (profiles/r01/README.md); lazy CT ranges with the split-tail schedule (N = 2^10:
   // 3 + 3 + 2 + 2, the polymul turn pass on 4-coefficient groups) when every modulus is
   // below 2^60; [0, 4q) Harvey ranges with 3 + 3 + 3 + 1 otherwise
-  if (p->lazy60 && lazy_enabled())
+  if (p->lazy60 && lazy_enabled()) {
+    if constexpr (LOGN == 10 && MODE == 2) {
+      const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
+      if (waves < RNT_TEAM4_WAVES)
+        return launch_warp_v<LOGN, MODE, 4, RNT_WARP_MINB / 2, false, 32, true, 4>(p, out, in, bop, bcast, batch, st);
+      if (waves < RNT_TEAM2_WAVES)
+        return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true, 2>(p, out, in, bop, bcast, batch, st);
+    }
     return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true>(p, out, in, bop, bcast, batch, st);
+  }
   return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 3>(p, out, in, bop, bcast, batch, st);
 }
 

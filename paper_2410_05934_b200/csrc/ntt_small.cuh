@@ -74,6 +74,16 @@ struct PassGeo {
   }
 };
 
+// A warp buffer is worked on by a team of TEAM warps (TEAM = 1: one warp, the
+// default).  The team's 32 TEAM lanes split every pass's groups; between passes
+// the team synchronises with __syncwarp (TEAM = 1) or, since a team larger than
+// one warp is a whole CTA, with __syncthreads.
+template <int TEAM>
+__device__ __forceinline__ void team_sync() {
+  if constexpr (TEAM == 1) __syncwarp();
+  else __syncthreads();
+}
+
 // K CT stages on x[0 .. 2^K) of one group; twiddle w[2^{S+v} + hi 2^v + blk].
 // LZ: lazy ranges for q < 2^60 (ct_bfly_lz; input canonical at stage 0).
 template <int S, int K, bool LZ = false, int S0 = 0>
@@ -165,13 +175,14 @@ constexpr int kToBufCanon = 2; // canonical values into the warp buffer
 // TWS: twiddle-table stride per polynomial of the warp (0: all polynomials
 // share T; 2^{n2}: row r + p of a 2^16 limb uses row table r + p).
 // S0: global index of local stage 0 (rows of a 2^16 limb: n1), for the LZ schedule.
-template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false, int S0 = 0>
+template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false, int S0 = 0, int TEAM = 1>
 __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
+  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL; ++gi) {
-    const Geo g(lane + 32 * gi);
+  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
+    const Geo g(lane + 32 * TEAM * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -197,18 +208,19 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
         buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = DST == kToBufCanon ? canon_fwd<LZ>(x[i], q, q2) : x[i];
     }
   }
-  __syncwarp();
+  team_sync<TEAM>();
 }
 
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, bool LAST, int TWS = 0, bool MIRROR = false,
-          bool LZT = false>
+          bool LZT = false, int TEAM = 1>
 __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                          u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
+  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL; ++gi) {
-    const Geo g(lane + 32 * gi);
+  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
+    const Geo g(lane + 32 * TEAM * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -233,21 +245,22 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
       for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
     }
   }
-  __syncwarp();
+  team_sync<TEAM>();
 }
 
 // Fused turn-around pass of the polymul: last CT pass -> (.) b_hat -> first
 // GS pass, all in registers.  b_hat comes from global memory (bview) or from
 // a second warp buffer holding canonical NTT(b) (BSRC == kFromBuf).
 template <int LOGN, int S, int K, int SRC, bool DST_GLOBAL, int BSRC, bool SCALE = true, int TWS = 0,
-          bool MIRROR = false, bool LZ = false, int S0 = 0>
+          bool MIRROR = false, bool LZ = false, int S0 = 0, int TEAM = 1>
 __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                           const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
+  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL; ++gi) {
-    const Geo g(lane + 32 * gi);
+  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
+    const Geo g(lane + 32 * TEAM * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -288,7 +301,7 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
       for (int i = 0; i < (1 << K); ++i) buf[pb + pad_off<LOGN, S, Geo::LO>(i)] = x[i];
     }
   }
-  __syncwarp();
+  team_sync<TEAM>();
 }
 
 // ---- full transforms on one warp buffer ---------------------------------------
@@ -313,20 +326,20 @@ static_assert(Passes<10, 3>::k(3) == 1 && Passes<10, 3>::s(3) == 9, "radix-8 sch
 
 // SRC0: source of the first pass (kFromGlobal, or kFromBuf for data already staged).
 template <int LOGN, int KM, int DST, bool SYNC = false, int TWS = 0, bool LZ = false, int S0 = 0,
-          int SRC0 = kFromGlobal>
+          int SRC0 = kFromGlobal, int TEAM = 1>
 __device__ __forceinline__ void warp_forward(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
   sfor<0, PS::NP>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
     constexpr int SRC = p == 0 ? SRC0 : kFromBuf;
     constexpr int D = p == PS::NP - 1 ? DST : kToBuf;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ, S0>(buf, src, dst, lane, T, q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), SRC, D, TWS, LZ, S0, TEAM>(buf, src, dst, lane, T, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
 
 template <int LOGN, int KM, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false, bool LZ = false,
-          int SRC0 = kFromGlobal>
+          int SRC0 = kFromGlobal, int TEAM = 1>
 __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int lane, const TW* T, TW s0, TW s1,
                                              u64 q, u64 q2) {
   using PS = Passes<LOGN, KM>;
@@ -334,33 +347,32 @@ __device__ __forceinline__ void warp_inverse(u64* buf, GView src, GView dst, int
     constexpr int i = decltype(I_)::value;
     constexpr int p = PS::NP - 1 - i;
     constexpr int SRC = i == 0 ? SRC0 : kFromBuf;
-    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE>(buf, src, dst, lane,
-                                                                                                T, s0, s1, q, q2);
+    inv_pass<LOGN, PS::s(p), PS::k(p), SRC, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE, TEAM>(
+        buf, src, dst, lane, T, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
 
 template <int LOGN, int KM, int BSRC, bool SYNC = false, bool SCALE = true, int TWS = 0, bool MIRROR = false,
-          bool LZ = false, int S0 = 0, int SRC0 = kFromGlobal>
+          bool LZ = false, int S0 = 0, int SRC0 = kFromGlobal, int TEAM = 1>
 __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GView bview, const u64* bbuf, int lane,
                                              const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using PS = Passes<LOGN, KM>;
   constexpr int NP = PS::NP;
   sfor<0, NP - 1>([&](auto P_) {
     constexpr int p = decltype(P_)::value;
-    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? SRC0 : kFromBuf, kToBuf, TWS, LZ, S0>(buf, src, dst, lane, Tf,
-                                                                                            q, q2);
+    fwd_pass<LOGN, PS::s(p), PS::k(p), p == 0 ? SRC0 : kFromBuf, kToBuf, TWS, LZ, S0, TEAM>(buf, src, dst, lane, Tf,
+                                                                                                  q, q2);
     if constexpr (SYNC) __syncthreads();
   });
   turn_pass<LOGN, PS::s(NP - 1), PS::k(NP - 1), NP == 1 ? SRC0 : kFromBuf, NP == 1, BSRC, SCALE, TWS, MIRROR,
-            LZ, S0>(
+            LZ, S0, TEAM>(
       buf, src, dst, bview, bbuf, lane, Tf, Ti, s0, s1, q, q2, qinv);
   if constexpr (SYNC) __syncthreads();
   sfor<0, NP - 1>([&](auto I_) {
     constexpr int p = NP - 2 - decltype(I_)::value;
-    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE>(buf, src, dst,
-                                                                                                     lane, Ti, s0, s1,
-                                                                                       q, q2);
+    inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, SCALE && p == 0, TWS, MIRROR, LZ && SCALE, TEAM>(
+        buf, src, dst, lane, Ti, s0, s1, q, q2);
     if constexpr (SYNC) __syncthreads();
   });
 }
@@ -371,20 +383,25 @@ __device__ __forceinline__ void warp_polymul(u64* buf, GView src, GView dst, GVi
 // (layout [B][L][N], reading C10).
 // MODE 0: forward, 1: inverse, 2: c = INTT(NTT(a) (.) b_hat), 3: c = INTT(NTT(a) (.) NTT(b)).
 // LZ: lazy CT ranges (ct_bfly_lz), valid when every modulus of the plan is < 2^60.
-template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false>
+// TEAM warps share one warp buffer (TEAM = 1: every warp owns its polynomials;
+// TEAM = 2 / 4: a team of warps splits each pass of one buffer -- more, shorter
+// work units, for batches that would leave the last wave of the GPU mostly empty).
+template <int LOGN, int MODE, int W = kTeamWarps, int MINB = 1, bool SYNC = false, int KM = 4, bool LZ = false,
+          int TEAM = 1>
 __global__ void __launch_bounds__(W * 32, MINB)
 k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_fwd, const TW* __restrict__ tw_inv, const LimbC* __restrict__ lc,
        uint32_t L, uint32_t B) {
   using C = WarpCfg<LOGN>;
   constexpr int N = C::N;
+  static_assert((TEAM == 1 || TEAM == W) && !(SYNC && TEAM > 1), "a team is one warp or the whole CTA");
   extern __shared__ __align__(16) u64 smem[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+  const int team = (int)(threadIdx.x >> 5) / TEAM;
+  const int lane = (int)threadIdx.x % (32 * TEAM);   // lane within the team
   const uint32_t l = blockIdx.y;
-  const uint64_t p0 = ((uint64_t)blockIdx.x * W + warp) * C::P;
-  if (!SYNC && p0 >= B) return;   // whole warp idle (warp-uniform); with SYNC idle warps run predicated
-  u64* buf = smem + (size_t)warp * kWarpBuf * (MODE == 3 ? 2 : 1);
+  const uint64_t p0 = ((uint64_t)blockIdx.x * (W / TEAM) + team) * C::P;
+  if (!SYNC && p0 >= B) return;   // whole team idle (team-uniform); with SYNC idle warps run predicated
+  u64* buf = smem + (size_t)team * kWarpBuf * (MODE == 3 ? 2 : 1);
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const uint64_t stride = (uint64_t)L * N;
   const GView src{in + (uint64_t)l * N, p0, stride, B};
@@ -393,25 +410,25 @@ k_warp(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Ti = tw_inv + (size_t)l * N;
   constexpr int SRC0 = kFromGlobal;
   if constexpr (MODE == 0) {
-    warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ, 0, SRC0>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<LOGN, KM, kToGlobal, SYNC, 0, LZ, 0, SRC0, TEAM>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<LOGN, KM, SYNC, true, 0, false, LZ, SRC0>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1, q,
-                                                           q2);
+    warp_inverse<LOGN, KM, SYNC, true, 0, false, LZ, SRC0, TEAM>(buf, src, dst, lane, Ti, lc[l].ninv, lc[l].ninv_w1,
+                                                                 q, q2);
   } else {
     const GView bview{bop + (uint64_t)l * N, b_bcast ? 0 : p0, b_bcast ? 0 : stride, b_bcast ? ~0ull : B};
     const u64 qinv = lc[l].qinv;
     if constexpr (MODE == 3) {
       u64* bbuf = buf + kWarpBuf;
       // canonical NTT(b) parked in the second warp buffer
-      warp_forward<LOGN, KM, kToBufCanon, SYNC, 0, LZ>(bbuf, bview, bview, lane, Tf, q, q2);
-      warp_polymul<LOGN, KM, kFromBuf, SYNC, true, 0, false, LZ>(buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+      warp_forward<LOGN, KM, kToBufCanon, SYNC, 0, LZ, 0, kFromGlobal, TEAM>(bbuf, bview, bview, lane, Tf, q, q2);
+      warp_polymul<LOGN, KM, kFromBuf, SYNC, true, 0, false, LZ, 0, kFromGlobal, TEAM>(
+          buf, src, dst, bview, bbuf, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     } else {
-      warp_polymul<LOGN, KM, kFromGlobal, SYNC, true, 0, false, LZ, 0, SRC0>(buf, src, dst, bview, nullptr, lane, Tf,
-                                                                         Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
+      warp_polymul<LOGN, KM, kFromGlobal, SYNC, true, 0, false, LZ, 0, SRC0, TEAM>(
+          buf, src, dst, bview, nullptr, lane, Tf, Ti, lc[l].ninvR, lc[l].ninvR_w1, q, q2, qinv);
     }
   }
 }
-
 
 // ---- TFHE external product ---------------------------------
 // c [n_slot][2][N] (RLWE pairs, one prime), rgsw_hat [2l][2][N] (NTT form, shared
@@ -623,9 +640,9 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
   }
 }
 
-template <int LOGN, int MODE, int W = kTeamWarps>
+template <int LOGN, int MODE, int W = kTeamWarps, int TEAM = 1>
 inline size_t warp_smem_bytes() {
-  return (size_t)W * kWarpBuf * 8 * (MODE == 3 ? 2 : 1);
+  return (size_t)(W / TEAM) * kWarpBuf * 8 * (MODE == 3 ? 2 : 1);
 }
 
 }  // namespace rnt

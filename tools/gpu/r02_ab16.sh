@@ -10,7 +10,7 @@ RNT_CLUSTER_UNITS=1000 python bench.py --steps 30 --no-cpu-baseline --no-e2e --n
 ncu --set full --clock-control none --import-source on -k regex:"k_col|k_row|k_cluster" -c 4 -o /tmp/r02d/prof16 python bench.py --workload cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph > $O/ncu16.log 2>&1
 RNT_CLUSTER_UNITS=1000 ncu --set full --clock-control none --import-source on -k regex:"k_cluster" -c 1 -o /tmp/r02d/profcl python bench.py --workload cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph > $O/ncucl.log 2>&1
 python tools/ncu_summary.py $O/ncu_16 /tmp/r02d/prof16.ncu-rep /tmp/r02d/profcl.ncu-rep > /dev/null 2>&1
-cp /tmp/r02d/*.ncu-rep $O/
+ls -la /tmp/r02d
 for f in $O/bench_*.json; do echo $f; python -c "
 import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['roofline']['frac'], [p['ms'] for p in d['parts']], d['digests_ok'])"; done
 ncu --set full --clock-control none --import-source on -k regex:"k_hrf" -c 1 -o /tmp/r02d/profhrf python bench.py --hrf --steps 1 --warmup 1 > $O/ncuhrf.log 2>&1
@@ -22,7 +22,7 @@ keys=[k for k in h if k.startswith('dram__') or 'lts__t_sectors_srcunit_tex_op_r
 for row in r[2:]:
     d=dict(zip(h,row)); print(d['Kernel Name'][:40]); [print(' ',k,d[k]) for k in keys]
 " > $O/hrf_dram.txt
-cp /tmp/r02d/profhrf.ncu-rep $O/
+
 for u in 8 2; do
 RNT_NVCC_EXTRA="-DRNT_HRF_UNROLL=$u" python -c "from paper_2410_05934_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
 python bench.py --hrf --steps 10 > $O/bench_hrf_u$u.json 2>&1
