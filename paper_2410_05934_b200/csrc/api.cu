@@ -261,14 +261,13 @@ static bool lazy_enabled() {
 #ifndef RNT_WARP_MINB
 #define RNT_WARP_MINB 12
 #endif
-// Team size by batch (N = 2^10 polymul units): a CTA of TEAM warps per polynomial
-// when the job fills fewer than RNT_TEAM{2,4}_WAVES waves of one-warp units
-// (experiments: -DRNT_TEAM2_WAVES=x / -DRNT_TEAM4_WAVES=x; 0 disables).
+// Team size by batch (N = 2^10 polymul units): a CTA of 2 warps per polynomial
+// when the job fills fewer than RNT_TEAM2_WAVES waves of one-warp units
+// (experiments: -DRNT_TEAM2_WAVES=x; 0 disables).  Measured (profiles/r02/teams):
+// cfg2 (1.15 waves) 0.0816 -> 0.0764 ms, cfg5 (4.6 waves) 0.2619 -> 0.2609 ms;
+// teams of 4 warps: cfg2 0.0763, cfg5 0.2673 ms (not built).
 #ifndef RNT_TEAM2_WAVES
-#define RNT_TEAM2_WAVES 0
-#endif
-#ifndef RNT_TEAM4_WAVES
-#define RNT_TEAM4_WAVES 0
+#define RNT_TEAM2_WAVES 8
 #endif
 
 template <int LOGN, int MODE>
@@ -281,8 +280,6 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   if (p->lazy60 && lazy_enabled()) {
     if constexpr (LOGN == 10 && MODE == 2) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
-      if (waves < RNT_TEAM4_WAVES)
-        return launch_warp_v<LOGN, MODE, 4, RNT_WARP_MINB / 2, false, 32, true, 4>(p, out, in, bop, bcast, batch, st);
       if (waves < RNT_TEAM2_WAVES)
         return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true, 2>(p, out, in, bop, bcast, batch, st);
     }
@@ -1104,9 +1101,14 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
 
 // HRF-MatVec (f4): one launch of k_hrf_matvec (hrf.cuh), a grid-stride loop
 // over the L N / 2 slot pairs, enough CTAs for every SM.  Experiments rebuild with
-// RNT_NVCC_EXTRA=-DRNT_HRF_UNROLL=n / -DRNT_HRF_CTAS_PER_SM=n (build.py).
+// RNT_NVCC_EXTRA=-DRNT_HRF_UNROLL=n / -DRNT_HRF_JS=n / -DRNT_HRF_CTAS_PER_SM=n (build.py).
+// Measured (N = 2^16, 4 limbs, n_slot 1024, JS = 1): unroll 2 / 4 / 8 = 0.658 / 0.585 /
+// 0.496 of HBM (memory-latency bound at 31 % warps active).
 #ifndef RNT_HRF_UNROLL
-#define RNT_HRF_UNROLL 4
+#define RNT_HRF_UNROLL 2
+#endif
+#ifndef RNT_HRF_JS
+#define RNT_HRF_JS 2
 #endif
 #ifndef RNT_HRF_CTAS_PER_SM
 #define RNT_HRF_CTAS_PER_SM 8
@@ -1136,11 +1138,11 @@ rnt_status rnt_hrf_matvec(rnt_plan p, uint64_t* out, const uint64_t* pt, const u
   }
   if (add && (s = debug_validate(p, add, 2, st)) != RNT_OK) return s;
   const uint64_t nvec = ln / 2;
-  const int threads = 256;
-  uint64_t blocks = (nvec + threads - 1) / threads;
+  constexpr int vb = 256 / RNT_HRF_JS;   // slot pairs per CTA
+  uint64_t blocks = (nvec + vb - 1) / vb;
   const uint64_t cap = (uint64_t)num_sms() * RNT_HRF_CTAS_PER_SM;
   if (blocks > cap) blocks = cap;
-  k_hrf_matvec<RNT_HRF_UNROLL><<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(pt),
+  k_hrf_matvec<RNT_HRF_UNROLL, RNT_HRF_JS><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(pt),
                                                         reinterpret_cast<const u64*>(ct), reinterpret_cast<const u64*>(add),
                                                         p->d_lc, n_slot, p->L, p->logn, nvec);
   return after_launch();

@@ -74,14 +74,26 @@ struct PassGeo {
   }
 };
 
-// A warp buffer is worked on by a team of TEAM warps (TEAM = 1: one warp, the
-// default).  The team's 32 TEAM lanes split every pass's groups; between passes
-// the team synchronises with __syncwarp (TEAM = 1) or, since a team larger than
-// one warp is a whole CTA, with __syncthreads.
+// A warp buffer is worked on by a team of warps (TEAM = 1: one warp, the
+// default).  The team's lanes split every pass's groups; between passes the team
+// synchronises with __syncwarp (one warp), __syncthreads (TEAM = 2, 4: the team is
+// the whole CTA) or a named barrier (TEAM = -2: teams of 2 warps inside a larger
+// CTA, barrier id 1 + warp / 2, 64 threads).
+template <int TEAM>
+struct Team {
+  static constexpr int size = TEAM > 0 ? TEAM : -TEAM;
+  static constexpr bool named = TEAM < 0;
+};
 template <int TEAM>
 __device__ __forceinline__ void team_sync() {
-  if constexpr (TEAM == 1) __syncwarp();
-  else __syncthreads();
+  if constexpr (Team<TEAM>::size == 1) {
+    __syncwarp();
+  } else if constexpr (Team<TEAM>::named) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x >> 5) / Team<TEAM>::size), "n"(32 * Team<TEAM>::size)
+                 : "memory");
+  } else {
+    __syncthreads();
+  }
 }
 
 // K CT stages on x[0 .. 2^K) of one group; twiddle w[2^{S+v} + hi 2^v + blk].
@@ -179,10 +191,11 @@ template <int LOGN, int S, int K, int SRC, int DST, int TWS = 0, bool LZ = false
 __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lane, const TW* T, u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
-  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
+  constexpr int TS = Team<TEAM>::size;
+  static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
-    const Geo g(lane + 32 * TEAM * gi);
+  for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
+    const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -217,10 +230,11 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
                                          u64 q, u64 q2) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
-  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
+  constexpr int TS = Team<TEAM>::size;
+  static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
-    const Geo g(lane + 32 * TEAM * gi);
+  for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
+    const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -257,10 +271,11 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
                                           const TW* Tf, const TW* Ti, TW s0, TW s1, u64 q, u64 q2, u64 qinv) {
   using Geo = PassGeo<LOGN, S, K>;
   constexpr int N = 1 << LOGN;
-  static_assert(Geo::GPL % TEAM == 0, "team splits the groups evenly");
+  constexpr int TS = Team<TEAM>::size;
+  static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
 #pragma unroll 1
-  for (int gi = 0; gi < Geo::GPL / TEAM; ++gi) {
-    const Geo g(lane + 32 * TEAM * gi);
+  for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
+    const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;
     const int pb = wpad(g.base);
     u64 x[1 << K];
@@ -630,7 +645,19 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
     smem[kWarpBuf + pe] = a1;
   }
   __syncthreads();
-  if (warp < 2) {
+  if constexpr (NW >= 4) {
+    // the two inverse NTTs on teams of two warps (warps 0-1: component 0, warps 2-3:
+    // component 1; named barriers), so the inverse phase takes half as long
+    if (warp < 4) {
+      const int team = warp >> 1;
+      const GView o{out + (uint64_t)team * N, s0, 2ull * N, n_slot};
+      sfor<0, NP>([&](auto I_) {
+        constexpr int p = NP - 1 - decltype(I_)::value;
+        inv_pass<LOGN, PS::s(p), PS::k(p), kFromBuf, p == 0, p == 0, 0, false, LZ, -2>(
+            smem + (size_t)team * kWarpBuf, o, o, (int)threadIdx.x & 63, tw_inv, lc[0].ninvR, lc[0].ninvR_w1, q, q2);
+      });
+    }
+  } else if (warp < 2) {
     const GView o{out + (uint64_t)warp * N, s0, 2ull * N, n_slot};
     sfor<0, NP>([&](auto I_) {
       constexpr int p = NP - 1 - decltype(I_)::value;

@@ -95,7 +95,7 @@ def _same_basis(a: RnsPoly, b: RnsPoly) -> None:
 
 def _same_shape(a: RnsPoly, o: RnsPoly) -> None:
     """`out` must hold exactly a's batch (the kernels write batch * L * N words)."""
-    _same_shape(a, o)
+    _same_basis(a, o)
     if o.batch != a.batch:
         raise ValueError(f"out batch {o.batch} != operand batch {a.batch}")
 
