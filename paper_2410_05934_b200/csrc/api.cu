@@ -269,6 +269,9 @@ static bool lazy_enabled() {
 #ifndef RNT_TEAM2_WAVES
 #define RNT_TEAM2_WAVES 8
 #endif
+#ifndef RNT_TEAM2_MINB
+#define RNT_TEAM2_MINB RNT_WARP_MINB
+#endif
 
 template <int LOGN, int MODE>
 static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
@@ -281,7 +284,7 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
     if constexpr (LOGN == 10 && MODE == 2) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
       if (waves < RNT_TEAM2_WAVES)
-        return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true, 2>(p, out, in, bop, bcast, batch, st);
+        return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, 32, true, 2>(p, out, in, bop, bcast, batch, st);
     }
     return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true>(p, out, in, bop, bcast, batch, st);
   }
@@ -438,10 +441,49 @@ static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
+// Dataflow polymul (k_flow, ntt_large.cuh): one persistent launch for the whole
+// NTT -> (.) -> INTT chain at N = 2^16.  Experiments rebuild with -DRNT_FLOW=0 for the
+// three-kernel chain.
+#ifndef RNT_FLOW
+#define RNT_FLOW 1
+#endif
+static bool flow_applies(const rnt_plan_s* p, int op) { return RNT_FLOW && p->logn == 16 && op == 2; }
+
+template <int LOGN>
+static rnt_status launch_flow(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
+                              uint32_t batch, cudaStream_t st) {
+  if constexpr (LOGN == 16) {
+    const uint64_t units = (uint64_t)batch * p->L;
+    const size_t words = 1 + 2 * units;
+    uint32_t* ctr = nullptr;
+    RNT_CUDA(cudaMallocAsync(&ctr, words * sizeof(uint32_t), st));
+    RNT_CUDA(cudaMemsetAsync(ctr, 0, words * sizeof(uint32_t), st));
+    constexpr size_t smem = flow_smem_bytes<LOGN>();
+    const bool lz = p->lazy60 && lazy_enabled();
+    auto kern = lz ? k_flow<LOGN, true> : k_flow<LOGN, false>;
+    static std::atomic<uint64_t> attr_lz{0}, attr{0};
+    if (rnt_status s = ensure_attr(kern, smem, lz ? attr_lz : attr); s != RNT_OK) return s;
+    int per_sm = 0;
+    RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    uint64_t grid = (uint64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+    const uint64_t tiles = 3ull * (TwoPass<LOGN>::R / kColTile) * units;
+    if (grid > tiles) grid = tiles;
+    kern<<<(unsigned)grid, 256, smem, st>>>(out, in, bop, bcast, p->d_col_fwd, p->d_col_inv, p->d_fwd, p->d_lc, p->L,
+                                             batch, ctr);
+    rnt_status s = after_launch();
+    cudaError_t e = cudaFreeAsync(ctr, st);
+    if (s == RNT_OK && e != cudaSuccess) return cuda_fail(e);
+    return s;
+  } else {
+    return RNT_E_INVALID_ARG;
+  }
+}
+
 template <int LOGN>
 static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
+  if (flow_applies(p, op)) return launch_flow<LOGN>(p, out, in, bop, bcast, batch, st);
   g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= 192;
   switch (op) {
     case 0:  // forward
@@ -1013,7 +1055,8 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   constexpr int split_g = 2;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   RNT_CUDA(cudaStreamIsCapturing(st, &cap));
-  if (cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
+  const bool flow = flow_applies(p, op == 3 ? 2 : op);
+  if (!flow && cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
     std::lock_guard<std::mutex> g(p->split_mu);
     for (int i = 0; i < split_g; ++i)
       if (!p->split[i]) RNT_CUDA(cudaStreamCreateWithFlags(&p->split[i], cudaStreamNonBlocking));
@@ -1102,13 +1145,15 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
 // HRF-MatVec (f4): one launch of k_hrf_matvec (hrf.cuh), a grid-stride loop
 // over the L N / 2 slot pairs, enough CTAs for every SM.  Experiments rebuild with
 // RNT_NVCC_EXTRA=-DRNT_HRF_UNROLL=n / -DRNT_HRF_JS=n / -DRNT_HRF_CTAS_PER_SM=n (build.py).
-// Measured (N = 2^16, 4 limbs, n_slot 1024, JS = 1): unroll 2 / 4 / 8 = 0.658 / 0.585 /
-// 0.496 of HBM (memory-latency bound at 31 % warps active).
+// Measured (N = 2^16, 4 limbs; fraction of HBM at n_slot 64 / 256 / 1024,
+// profiles/r02/hrf): unroll 4, JS 1: 0.51 / 0.57 / 0.59 (31 % warps active, long-scoreboard
+// bound); unroll 2, JS 2: 0.71 / 0.86 / 0.90; unroll 1, JS 4: 0.71 / 0.90 / 0.96;
+// unroll 2, JS 1, min 4 CTAs/SM (<= 64 registers): 0.79 / 0.92 / 0.95 -- shipped.
 #ifndef RNT_HRF_UNROLL
 #define RNT_HRF_UNROLL 2
 #endif
 #ifndef RNT_HRF_JS
-#define RNT_HRF_JS 2
+#define RNT_HRF_JS 1
 #endif
 #ifndef RNT_HRF_CTAS_PER_SM
 #define RNT_HRF_CTAS_PER_SM 8

@@ -65,7 +65,7 @@ __device__ __forceinline__ void acc_add(Acc192& a, const Acc192& b) {
 // through shared memory before the reduction.  Grid-stride over slot-pair blocks.
 // Thread v owns slots 2v, 2v + 1 of limb (2v) >> logn.
 #ifndef RNT_HRF_MINB
-#define RNT_HRF_MINB 1
+#define RNT_HRF_MINB 4
 #endif
 template <int UNROLL, int JS>
 __global__ void __launch_bounds__(256, RNT_HRF_MINB)

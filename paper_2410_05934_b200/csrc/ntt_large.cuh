@@ -64,28 +64,37 @@ __device__ __forceinline__ int row_swz(int c) {
 // lifts it to q_t on load: x mod q_t = x - q_t if x >= q_t (requires q_j < 2 q_t).
 // LZ: lazy CT ranges (modarith.cuh ct_bfly_lz, plan flag lazy60); the output
 // then carries the LZ bound of stage n1 and must feed an LZ row pass.
-template <int LOGN, int CT = kColTile, bool MODUP = false, bool LZ = false>
-__global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
-k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
-          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+// Global loads of data another CTA of the same launch may have written (the
+// dataflow kernel k_flow) bypass L1 (ld.global.cg); the stand-alone kernels use
+// plain loads.
+template <bool CG>
+__device__ __forceinline__ u64 ld_data(const u64* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+// One pass-1 tile: columns [bx CT, bx CT + CT) of unit y (y = limb * B + poly,
+// limb-major CTA order); `tile` is R * CT words of shared memory.
+template <int LOGN, int CT, bool MODUP, bool LZ, bool CG = false>
+__device__ __forceinline__ void col_fwd_tile(u64* __restrict__ out, const u64* __restrict__ in,
+                                             const TW* __restrict__ tw_col, const LimbC* __restrict__ lc, uint32_t L,
+                                             uint32_t B, uint64_t y, int bx, u64* tile) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 tile[P::R * CT];
   const int c = threadIdx.x % CT;
   const int r0 = threadIdx.x / CT;
-  const uint64_t y = y0 + blockIdx.y;          // y = limb * B + poly (limb-major CTA order)
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const TW* T = tw_col + (size_t)l * P::R;
-  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)bx * CT + c;
   u64 x[kEl];
   if constexpr (MODUP) {
-    const size_t ibase = (y % B) * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
+    const size_t ibase = (y % B) * (size_t)(P::R * P::Cn) + (size_t)bx * CT + c;
 #pragma unroll
     for (int i = 0; i < kEl; ++i) x[i] = csub(__ldg(in + ibase + (size_t)(r0 + P::T1 * i) * P::Cn), q);
   } else {
 #pragma unroll
-    for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(r0 + P::T1 * i) * P::Cn];
+    for (int i = 0; i < kEl; ++i) x[i] = ld_data<CG>(in + base + (size_t)(r0 + P::T1 * i) * P::Cn);
   }
   // sub-pass A: stages 0..3, twiddle w[2^s + (i >> (4-s))] (uniform)
   sfor<0, 4>([&](auto S_) {
@@ -120,24 +129,30 @@ k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
   for (int i = 0; i < kEl; ++i) out[base + (size_t)(kEl * r1 + i) * P::Cn] = x[i];
 }
 
-// Inverse: GS stages n1-1..0 (+ N^{-1} or N^{-1} R scaling), canonical output.
-template <int LOGN, int CT = kColTile>
+template <int LOGN, int CT = kColTile, bool MODUP = false, bool LZ = false>
 __global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
-k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
-          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
+k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
+          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+  __shared__ __align__(16) u64 tile[TwoPass<LOGN>::R * CT];
+  col_fwd_tile<LOGN, CT, MODUP, LZ>(out, in, tw_col, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, tile);
+}
+
+// Inverse: GS stages n1-1..0 (+ N^{-1} or N^{-1} R scaling), canonical output.
+template <int LOGN, int CT, bool CG = false>
+__device__ __forceinline__ void col_inv_tile(u64* __restrict__ out, const u64* __restrict__ in,
+                                             const TW* __restrict__ tw_col, const LimbC* __restrict__ lc, uint32_t L,
+                                             uint32_t B, uint64_t y, int bx, int after_mont, u64* tile) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 tile[P::R * CT];
   const int c = threadIdx.x % CT;
   const int r1 = threadIdx.x / CT;
-  const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const TW* T = tw_col + (size_t)l * P::R;
-  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)blockIdx.x * CT + c;
+  const size_t base = u * (size_t)(P::R * P::Cn) + (size_t)bx * CT + c;
   u64 x[kEl];
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) x[i] = in[base + (size_t)(kEl * r1 + i) * P::Cn];
+  for (int i = 0; i < kEl; ++i) x[i] = ld_data<CG>(in + base + (size_t)(kEl * r1 + i) * P::Cn);
   sfor<0, P::n1 - 4>([&](auto I_) {
     constexpr int s = P::n1 - 1 - decltype(I_)::value;
     constexpr int t = P::R >> (s + 1);
@@ -170,6 +185,14 @@ k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restric
   for (int k = 0; k < kEl / 2; ++k) gs_bfly_last(x[k], x[k + kEl / 2], s0, s1, q, q2);
 #pragma unroll
   for (int i = 0; i < kEl; ++i) out[base + (size_t)(r0 + P::T1 * i) * P::Cn] = canon2(x[i], q);
+}
+
+template <int LOGN, int CT = kColTile>
+__global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
+k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
+          const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
+  __shared__ __align__(16) u64 tile[TwoPass<LOGN>::R * CT];
+  col_inv_tile<LOGN, CT>(out, in, tw_col, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, after_mont, tile);
 }
 
 // ============================== pass 2 (rows) =================================
@@ -274,12 +297,12 @@ __device__ __forceinline__ void row_B_to_A(u64 (&x)[kEl], u64* rb, int c0) {
 #else
 #define RNT_ROW_BOUNDS(t) __launch_bounds__(t)
 #endif
-template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC, bool LZ = false>
-__global__ void RNT_ROW_BOUNDS(RPC_ * TwoPass<LOGN>::T2)
-k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
-      const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+// One pass-2 tile: RPC_ rows (block rx) of unit y; `sbuf` is RPC_ ROWBUF words.
+template <int LOGN, int MODE, int RPC_, bool LZ, bool CG = false>
+__device__ __forceinline__ void row_tile(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop,
+                                         int b_bcast, const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc,
+                                         uint32_t L, uint32_t B, uint64_t y, int rx, u64* sbuf) {
   using P = TwoPass<LOGN>;
-  __shared__ __align__(16) u64 sbuf[RPC_ * P::ROWBUF];
   const int c0 = threadIdx.x % P::T2;
   const int rr = threadIdx.x / P::T2;
   // With 16 threads per row a warp holds two rows: make them r and R-1-r, so
@@ -287,12 +310,11 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   // partner half-warp just loaded.
   int r;
   if constexpr (P::T2 == 16 && RPC_ % 2 == 0) {
-    const int pi = blockIdx.x * (RPC_ / 2) + (rr >> 1);
+    const int pi = rx * (RPC_ / 2) + (rr >> 1);
     r = (rr & 1) ? (P::R - 1 - pi) : pi;
   } else {
-    r = blockIdx.x * RPC_ + rr;
+    r = rx * RPC_ + rr;
   }
-  const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
   const u64 q = lc[l].q, q2 = lc[l].q2;
@@ -302,7 +324,7 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   const TW* Tm = tw_row_fwd + ((size_t)l * P::R + (P::R - 1 - r)) * P::Cn;   // mirrored row
   u64 x[kEl];
 #pragma unroll
-  for (int i = 0; i < kEl; ++i) x[i] = in[rowoff + c0 + P::T2 * i];
+  for (int i = 0; i < kEl; ++i) x[i] = ld_data<CG>(in + rowoff + c0 + P::T2 * i);
   if (MODE == 1) {
     row_A_to_B<LOGN>(x, rb, c0);
     row_inv_B<LOGN>(x, Tm, c0, q, q2);
@@ -336,6 +358,14 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
   }
 #pragma unroll
   for (int i = 0; i < kEl; ++i) out[rowoff + c0 + P::T2 * i] = x[i];
+}
+
+template <int LOGN, int MODE, int RPC_ = TwoPass<LOGN>::RPC, bool LZ = false>
+__global__ void RNT_ROW_BOUNDS(RPC_ * TwoPass<LOGN>::T2)
+k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
+      const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
+  __shared__ __align__(16) u64 sbuf[RPC_ * TwoPass<LOGN>::ROWBUF];
+  row_tile<LOGN, MODE, RPC_, LZ>(out, in, bop, b_bcast, tw_row_fwd, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, sbuf);
 }
 
 // ============================ pass 2 + key product ============================
@@ -447,6 +477,84 @@ k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
                                                                              none,
                                                                   none, q, q2, lc[l].qinv);
   }
+}
+
+// ====================== dataflow polymul (one persistent launch) ======================
+// c = INTT(NTT(a) (.) b_hat) for every unit of a batch at N = 2^11 .. 2^16 in ONE
+// launch instead of three: persistent CTAs take tickets from a global counter;
+// ticket -> (phase, unit, tile) in virtual rounds of 3 x T slots, round r holding the
+// pass-1 tiles of unit r, the pass-2 tiles of unit r - D and the inverse pass-1 tiles
+// of unit r - 2D (T = R / kColTile = R / RPC tiles per phase).  A tile of phase k > 0
+// waits (thread 0 spins on an acquire load, __nanosleep back-off) until all T tiles of
+// phase k - 1 of its unit are counted done; a finished tile is counted after a CTA
+// barrier and a __threadfence (release).  Every dependency points to a smaller ticket,
+// already taken by a running CTA, so the spin always ends, whatever the residency.
+// No phase boundary leaves SMs idle (the three-kernel chain idled ~37 % of the column
+// kernels' time on ramps and tails at cfg3, profiles/r02/ab16) and the phases of
+// different units overlap.  Intermediates are read with ld.global.cg (other SMs wrote
+// them during this launch).  ctr: [1 + 2 U] zeroed words (ticket, done counts).
+constexpr int kFlowLag = 7;   // D: rounds between a tile and the tiles it waits for
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int LOGN, bool LZ>
+__global__ void __launch_bounds__(256, 2)
+k_flow(u64* out, const u64* in, const u64* __restrict__ bop, int b_bcast, const TW* __restrict__ tw_col_fwd,
+       const TW* __restrict__ tw_col_inv, const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc,
+       uint32_t L, uint32_t B, uint32_t* ctr) {
+  using P = TwoPass<LOGN>;
+  static_assert(P::P1_THREADS == 256 && P::P2_THREADS == 256, "one CTA shape for both passes");
+  constexpr int T = P::R / kColTile;                 // tiles per phase (columns and rows alike)
+  static_assert(P::R / P::RPC == T, "same tile count per phase");
+  extern __shared__ __align__(16) u64 fsm[];
+  __shared__ uint32_t s_ticket;
+  const uint64_t U = (uint64_t)B * L;
+  const uint64_t rounds = U + 2 * kFlowLag;
+  uint32_t* done0 = ctr + 1;
+  uint32_t* done1 = ctr + 1 + U;
+  for (;;) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const uint64_t t = s_ticket;
+    __syncthreads();
+    const uint64_t r = t / (3 * T);
+    if (r >= rounds) break;
+    const int slot = (int)(t % (3 * T));
+    const int phase = slot / T, tile = slot % T;
+    const int64_t unit = (int64_t)r - (int64_t)phase * kFlowLag;
+    if (unit < 0 || unit >= (int64_t)U) continue;     // empty slot of a ramp round (CTA-uniform)
+    const uint64_t y = (uint64_t)unit;
+    if (phase > 0) {
+      if (threadIdx.x == 0) {
+        const uint32_t* dep = (phase == 1 ? done0 : done1) + y;
+        while (ld_acquire_u32(dep) < (uint32_t)T) __nanosleep(100);
+      }
+      __syncthreads();
+    }
+    if (phase == 0) {
+      col_fwd_tile<LOGN, kColTile, false, LZ, true>(out, in, tw_col_fwd, lc, L, B, y, tile, fsm);
+    } else if (phase == 1) {
+      row_tile<LOGN, 2, P::RPC, LZ, true>(out, out, bop, b_bcast, tw_row_fwd, lc, L, B, y, tile, fsm);
+    } else {
+      col_inv_tile<LOGN, kColTile, true>(out, out, tw_col_inv, lc, L, B, y, tile, 1, fsm);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && phase < 2) {
+      __threadfence();
+      atomicAdd((phase == 0 ? done0 : done1) + y, 1u);
+    }
+  }
+}
+
+template <int LOGN>
+constexpr size_t flow_smem_bytes() {
+  using P = TwoPass<LOGN>;
+  constexpr size_t a = (size_t)P::R * kColTile * 8, b = (size_t)P::RPC * P::ROWBUF * 8;
+  return a > b ? a : b;
 }
 
 }  // namespace rnt
