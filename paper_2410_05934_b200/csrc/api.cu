@@ -109,10 +109,17 @@ __global__ void k_pointwise(u64* __restrict__ c, const u64* __restrict__ a, cons
   }
 }
 
-// Galois automorphism sigma_g (rnt_automorph).  One thread per output slot;
-// gathers from the same limb (L2-resident for N <= 2^16).
+// Galois automorphism sigma_g (rnt_automorph).
 //   NTT form:  out[k] = in[pi(k)],  2 brv(pi(k)) + 1 = (2 brv(k) + 1) g mod 2N
 //   coeff form: out[j] = +-in[j g^{-1} mod 2N] (sign when the source index >= N)
+// Scatter formulation (default): a thread reads in[e] (coalesced) and writes it to its
+// destination -- pi^{-1} is the same map with g^{-1}, and coefficient i goes to i g mod
+// 2N (negated past N) -- so the loads never stall on a gather; the 8-byte scattered
+// stores merge into sectors in L2.  RNT_AUTOMORPH_SCATTER=0 (experiment builds) keeps the
+// gather form.  One limb is 8N bytes (512 KB at 2^16): L2-resident while it is permuted.
+#ifndef RNT_AUTOMORPH_SCATTER
+#define RNT_AUTOMORPH_SCATTER 1
+#endif
 __global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, const LimbC* __restrict__ lc,
                             uint32_t L, uint32_t logn, uint32_t g, uint32_t ginv, int ntt_domain, uint64_t total) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -120,6 +127,23 @@ __global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, c
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
     const uint64_t u = e >> logn;
     const uint32_t k = (uint32_t)(e & (n - 1));
+#if RNT_AUTOMORPH_SCATTER
+    const u64 x = __ldcs(in + e);
+    u64* dst = out + (u << logn);
+    if (ntt_domain) {
+      const uint32_t ek = 2u * (__brev(k) >> (32 - logn)) + 1u;
+      const uint32_t es = (uint32_t)(((uint64_t)ek * ginv) & mask2n);
+      dst[__brev((es - 1u) >> 1) >> (32 - logn)] = x;
+    } else {
+      const uint32_t t = (uint32_t)(((uint64_t)k * g) & mask2n);
+      if (t < n) {
+        dst[t] = x;
+      } else {
+        const u64 q = lc[u % L].q;
+        dst[t - n] = x ? q - x : 0ull;
+      }
+    }
+#else
     const u64* src = in + (u << logn);
     u64 v;
     if (ntt_domain) {
@@ -138,6 +162,7 @@ __global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, c
       }
     }
     out[e] = v;
+#endif
   }
 }
 
@@ -441,49 +466,10 @@ static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
-// Dataflow polymul (k_flow, ntt_large.cuh): one persistent launch for the whole
-// NTT -> (.) -> INTT chain at N = 2^16.  Experiments rebuild with -DRNT_FLOW=0 for the
-// three-kernel chain.
-#ifndef RNT_FLOW
-#define RNT_FLOW 1
-#endif
-static bool flow_applies(const rnt_plan_s* p, int op) { return RNT_FLOW && p->logn == 16 && op == 2; }
-
-template <int LOGN>
-static rnt_status launch_flow(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
-                              uint32_t batch, cudaStream_t st) {
-  if constexpr (LOGN == 16) {
-    const uint64_t units = (uint64_t)batch * p->L;
-    const size_t words = 1 + 2 * units;
-    uint32_t* ctr = nullptr;
-    RNT_CUDA(cudaMallocAsync(&ctr, words * sizeof(uint32_t), st));
-    RNT_CUDA(cudaMemsetAsync(ctr, 0, words * sizeof(uint32_t), st));
-    constexpr size_t smem = flow_smem_bytes<LOGN>();
-    const bool lz = p->lazy60 && lazy_enabled();
-    auto kern = lz ? k_flow<LOGN, true> : k_flow<LOGN, false>;
-    static std::atomic<uint64_t> attr_lz{0}, attr{0};
-    if (rnt_status s = ensure_attr(kern, smem, lz ? attr_lz : attr); s != RNT_OK) return s;
-    int per_sm = 0;
-    RNT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    uint64_t grid = (uint64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
-    const uint64_t tiles = 3ull * (TwoPass<LOGN>::R / kColTile) * units;
-    if (grid > tiles) grid = tiles;
-    kern<<<(unsigned)grid, 256, smem, st>>>(out, in, bop, bcast, p->d_col_fwd, p->d_col_inv, p->d_fwd, p->d_lc, p->L,
-                                             batch, ctr);
-    rnt_status s = after_launch();
-    cudaError_t e = cudaFreeAsync(ctr, st);
-    if (s == RNT_OK && e != cudaSuccess) return cuda_fail(e);
-    return s;
-  } else {
-    return RNT_E_INVALID_ARG;
-  }
-}
-
 template <int LOGN>
 static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
-  if (flow_applies(p, op)) return launch_flow<LOGN>(p, out, in, bop, bcast, batch, st);
   g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= 192;
   switch (op) {
     case 0:  // forward
@@ -1055,8 +1041,7 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   constexpr int split_g = 2;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   RNT_CUDA(cudaStreamIsCapturing(st, &cap));
-  const bool flow = flow_applies(p, op == 3 ? 2 : op);
-  if (!flow && cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
+  if (cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
     std::lock_guard<std::mutex> g(p->split_mu);
     for (int i = 0; i < split_g; ++i)
       if (!p->split[i]) RNT_CUDA(cudaStreamCreateWithFlags(&p->split[i], cudaStreamNonBlocking));

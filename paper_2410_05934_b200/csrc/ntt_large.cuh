@@ -64,9 +64,9 @@ __device__ __forceinline__ int row_swz(int c) {
 // lifts it to q_t on load: x mod q_t = x - q_t if x >= q_t (requires q_j < 2 q_t).
 // LZ: lazy CT ranges (modarith.cuh ct_bfly_lz, plan flag lazy60); the output
 // then carries the LZ bound of stage n1 and must feed an LZ row pass.
-// Global loads of data another CTA of the same launch may have written (the
-// dataflow kernel k_flow) bypass L1 (ld.global.cg); the stand-alone kernels use
-// plain loads.
+// CG = true: data loads bypass L1 (ld.global.cg), for callers that read data another
+// CTA of the same launch wrote (a round-2 single-launch dataflow experiment, see
+// DESIGN.md KB2); the stand-alone kernels use plain loads.
 template <bool CG>
 __device__ __forceinline__ u64 ld_data(const u64* p) {
   if constexpr (CG) return __ldcg(p);
@@ -477,84 +477,6 @@ k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
                                                                              none,
                                                                   none, q, q2, lc[l].qinv);
   }
-}
-
-// ====================== dataflow polymul (one persistent launch) ======================
-// c = INTT(NTT(a) (.) b_hat) for every unit of a batch at N = 2^11 .. 2^16 in ONE
-// launch instead of three: persistent CTAs take tickets from a global counter;
-// ticket -> (phase, unit, tile) in virtual rounds of 3 x T slots, round r holding the
-// pass-1 tiles of unit r, the pass-2 tiles of unit r - D and the inverse pass-1 tiles
-// of unit r - 2D (T = R / kColTile = R / RPC tiles per phase).  A tile of phase k > 0
-// waits (thread 0 spins on an acquire load, __nanosleep back-off) until all T tiles of
-// phase k - 1 of its unit are counted done; a finished tile is counted after a CTA
-// barrier and a __threadfence (release).  Every dependency points to a smaller ticket,
-// already taken by a running CTA, so the spin always ends, whatever the residency.
-// No phase boundary leaves SMs idle (the three-kernel chain idled ~37 % of the column
-// kernels' time on ramps and tails at cfg3, profiles/r02/ab16) and the phases of
-// different units overlap.  Intermediates are read with ld.global.cg (other SMs wrote
-// them during this launch).  ctr: [1 + 2 U] zeroed words (ticket, done counts).
-constexpr int kFlowLag = 7;   // D: rounds between a tile and the tiles it waits for
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int LOGN, bool LZ>
-__global__ void __launch_bounds__(256, 2)
-k_flow(u64* out, const u64* in, const u64* __restrict__ bop, int b_bcast, const TW* __restrict__ tw_col_fwd,
-       const TW* __restrict__ tw_col_inv, const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc,
-       uint32_t L, uint32_t B, uint32_t* ctr) {
-  using P = TwoPass<LOGN>;
-  static_assert(P::P1_THREADS == 256 && P::P2_THREADS == 256, "one CTA shape for both passes");
-  constexpr int T = P::R / kColTile;                 // tiles per phase (columns and rows alike)
-  static_assert(P::R / P::RPC == T, "same tile count per phase");
-  extern __shared__ __align__(16) u64 fsm[];
-  __shared__ uint32_t s_ticket;
-  const uint64_t U = (uint64_t)B * L;
-  const uint64_t rounds = U + 2 * kFlowLag;
-  uint32_t* done0 = ctr + 1;
-  uint32_t* done1 = ctr + 1 + U;
-  for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint64_t t = s_ticket;
-    __syncthreads();
-    const uint64_t r = t / (3 * T);
-    if (r >= rounds) break;
-    const int slot = (int)(t % (3 * T));
-    const int phase = slot / T, tile = slot % T;
-    const int64_t unit = (int64_t)r - (int64_t)phase * kFlowLag;
-    if (unit < 0 || unit >= (int64_t)U) continue;     // empty slot of a ramp round (CTA-uniform)
-    const uint64_t y = (uint64_t)unit;
-    if (phase > 0) {
-      if (threadIdx.x == 0) {
-        const uint32_t* dep = (phase == 1 ? done0 : done1) + y;
-        while (ld_acquire_u32(dep) < (uint32_t)T) __nanosleep(100);
-      }
-      __syncthreads();
-    }
-    if (phase == 0) {
-      col_fwd_tile<LOGN, kColTile, false, LZ, true>(out, in, tw_col_fwd, lc, L, B, y, tile, fsm);
-    } else if (phase == 1) {
-      row_tile<LOGN, 2, P::RPC, LZ, true>(out, out, bop, b_bcast, tw_row_fwd, lc, L, B, y, tile, fsm);
-    } else {
-      col_inv_tile<LOGN, kColTile, true>(out, out, tw_col_inv, lc, L, B, y, tile, 1, fsm);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && phase < 2) {
-      __threadfence();
-      atomicAdd((phase == 0 ? done0 : done1) + y, 1u);
-    }
-  }
-}
-
-template <int LOGN>
-constexpr size_t flow_smem_bytes() {
-  using P = TwoPass<LOGN>;
-  constexpr size_t a = (size_t)P::R * kColTile * 8, b = (size_t)P::RPC * P::ROWBUF * 8;
-  return a > b ? a : b;
 }
 
 }  // namespace rnt
