@@ -773,8 +773,12 @@ static void bconv_tables(const uint64_t* q, uint32_t L, const uint64_t* p, uint3
 // column pass with the lift on load (k_col_fwd<.., MODUP>), then the row pass
 // with the key multiply-accumulate (k_row_mac).  E: [dnum][LK][N] scratch.
 // Digit split of the fused key product (k_row_mac blockIdx.z): dnum digits in
-// `split` partial sums, added by k_ks_sum (2..5 measured no faster: 1).
-static uint32_t ks_split(uint32_t dnum) { return dnum ? 1u : 0u; }
+// `split` partial sums, added by k_ks_sum (round 1: 2..5 measured no faster; experiment
+// builds: -DRNT_KS_SPLIT=n).
+#ifndef RNT_KS_SPLIT
+#define RNT_KS_SPLIT 1
+#endif
+static uint32_t ks_split(uint32_t dnum) { return dnum < RNT_KS_SPLIT ? dnum : RNT_KS_SPLIT; }
 
 template <int LOGN, bool LZ>
 static rnt_status ks_fused_launch_v(const rnt_plan_s* qp, u64* u, u64* E, const u64* x, const u64* evk,

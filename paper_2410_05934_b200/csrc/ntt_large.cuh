@@ -377,8 +377,16 @@ k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__
 // the NTT-form extended polynomials never go back to HBM.  Montgomery
 // products, accumulators kept in [0, 2q); u written canonical.
 // (min-blocks 2: the LZ variant compiled to 130 registers, one CTA per SM)
+// (RNT_ROWMAC_MINB, RNT_ROWMAC_PREFETCH: experiment builds; PREFETCH loads digit
+// j + 1's rows of E into registers while digit j's row stages run.)
+#ifndef RNT_ROWMAC_MINB
+#define RNT_ROWMAC_MINB 2
+#endif
+#ifndef RNT_ROWMAC_PREFETCH
+#define RNT_ROWMAC_PREFETCH 0
+#endif
 template <int LOGN, int RPC_, bool LZ = false>
-__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2, 2)
+__global__ void __launch_bounds__(RPC_ * TwoPass<LOGN>::T2, RNT_ROWMAC_MINB)
 k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict__ evk,
           const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t LK, uint32_t dnum,
           uint32_t dsplit) {
@@ -402,11 +410,29 @@ k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict
   const size_t roff = (size_t)r * P::Cn + c0;
   const uint32_t jb = blockIdx.z * dnum / dsplit, je = (blockIdx.z + 1) * dnum / dsplit;
   uo += (size_t)blockIdx.z * 2 * LK * N;
+#if RNT_ROWMAC_PREFETCH
+  u64 nx[kEl];
+  if (jb < je) {
+    const u64* src = E + ((size_t)jb * LK + t) * N + roff;
+#pragma unroll
+    for (int i = 0; i < kEl; ++i) nx[i] = __ldcs(src + P::T2 * i);
+  }
+#endif
   for (uint32_t j = jb; j < je; ++j) {
-    const u64* src = E + ((size_t)j * LK + t) * N + roff;
     u64 x[kEl];
+#if RNT_ROWMAC_PREFETCH
+#pragma unroll
+    for (int i = 0; i < kEl; ++i) x[i] = nx[i];
+    if (j + 1 < je) {
+      const u64* nsrc = E + ((size_t)(j + 1) * LK + t) * N + roff;
+#pragma unroll
+      for (int i = 0; i < kEl; ++i) nx[i] = __ldcs(nsrc + P::T2 * i);
+    }
+#else
+    const u64* src = E + ((size_t)j * LK + t) * N + roff;
 #pragma unroll
     for (int i = 0; i < kEl; ++i) x[i] = __ldcs(src + P::T2 * i);
+#endif
     row_fwd_A<LOGN, LZ>(x, Tf, q, q2);
     row_A_to_B<LOGN>(x, rb, c0);
     row_fwd_B<LOGN, LZ>(x, Tf, c0, q, q2);

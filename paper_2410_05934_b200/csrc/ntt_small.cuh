@@ -26,6 +26,13 @@ namespace rnt {
 
 constexpr int kWarpElems = 1024;          // coefficients per warp buffer
 constexpr int kTeamWarps = 4;             // warps per CTA
+// Group-loop unroll of the 4-coefficient (K = 2) passes: 2 groups per iteration give
+// each stage 4 independent butterflies instead of 2 (experiment builds:
+// -DRNT_K2_UNROLL=n; the 8-coefficient passes stay rolled for the register budget).
+#ifndef RNT_K2_UNROLL
+#define RNT_K2_UNROLL 1
+#endif
+constexpr int kK2Unroll = RNT_K2_UNROLL;
 
 template <int LOGN>
 struct WarpCfg {
@@ -193,7 +200,7 @@ __device__ __forceinline__ void fwd_pass(u64* buf, GView src, GView dst, int lan
   constexpr int N = 1 << LOGN;
   constexpr int TS = Team<TEAM>::size;
   static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
-#pragma unroll 1
+#pragma unroll(K == 2 ? kK2Unroll : 1)
   for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
     const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;
@@ -232,7 +239,7 @@ __device__ __forceinline__ void inv_pass(u64* buf, GView src, GView dst, int lan
   constexpr int N = 1 << LOGN;
   constexpr int TS = Team<TEAM>::size;
   static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
-#pragma unroll 1
+#pragma unroll(K == 2 ? kK2Unroll : 1)
   for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
     const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;
@@ -273,7 +280,7 @@ __device__ __forceinline__ void turn_pass(u64* buf, GView src, GView dst, GView 
   constexpr int N = 1 << LOGN;
   constexpr int TS = Team<TEAM>::size;
   static_assert(Geo::GPL % TS == 0, "team splits the groups evenly");
-#pragma unroll 1
+#pragma unroll(K == 2 ? kK2Unroll : 1)
   for (int gi = 0; gi < Geo::GPL / TS; ++gi) {
     const Geo g(lane + 32 * TS * gi);
     const int jj0 = g.base - g.poly * N;

@@ -77,5 +77,14 @@ o3 = torch.empty(c.shape, dtype=torch.int64, device="cuda")
 R.external_product(p, o3, dev(c), dev(z), 20, 3)
 ok &= all(np.array_equal(host(o3)[s_], O.external_product(c[s_], z, ps[0], O.min_psi(ps[0], 10), 20, 3))
           for s_ in range(3))
+# HRF-MatVec (f4), N = 2^12, 2 limbs, 5 slots, with the "+ b" term
+ps = O.primes(12, 2)
+p = R.Plan(12, ps)
+pt = inputs.residues(9, 5, ps, 1 << 12)
+ct = inputs.residues(10, 10, ps, 1 << 12).reshape(5, 2, 2, 1 << 12)
+ad = inputs.residues(11, 2, ps, 1 << 12)
+o4 = torch.empty((2, 2, 1 << 12), dtype=torch.int64, device="cuda")
+R.hrf_matvec(p, o4, dev(pt), dev(ct), add=dev(ad))
+ok &= np.array_equal(host(o4), O.hrf_matvec(pt, ct, ps, add=ad))
 torch.cuda.synchronize()
 print("sanitize run ok" if ok else "MISMATCH")
