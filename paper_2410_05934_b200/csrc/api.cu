@@ -385,6 +385,14 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // 0.827 -> 0.804 ms); smaller jobs the 16-column tiles and k_row (k_rows
 // under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
 static thread_local bool g_large_wide = false;   // set by large_op for the current call
+// Experiment builds: -DRNT_WIDE_UNITS=n (limb-units from which the wide path is taken),
+// -DRNT_ROWS_TEAM=2 (k_rows with 2-warp teams).
+#ifndef RNT_WIDE_UNITS
+#define RNT_WIDE_UNITS 192
+#endif
+#ifndef RNT_ROWS_TEAM
+#define RNT_ROWS_TEAM 1
+#endif
 
 template <int LOGN, int CT, bool LZ = false>
 static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
@@ -432,20 +440,21 @@ static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, con
   return RNT_OK;
 }
 
-template <int LOGN, int MODE, bool LZ = false>
+template <int LOGN, int MODE, bool LZ = false, int TEAM = 1>
 static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                    uint32_t batch, cudaStream_t st) {
   using P = TwoPass<LOGN>;
   static std::atomic<uint64_t> attr{0};
-  const size_t smem = (size_t)kRowWarps * kWarpBuf * 8;
-  if (rnt_status s = ensure_attr(k_rows<LOGN, MODE, LZ>, smem, attr); s != RNT_OK) return s;
-  constexpr int rows_per_cta = kRowWarps * (kWarpElems / P::Cn);
+  auto kern = k_rows<LOGN, MODE, LZ, TEAM>;
+  const size_t smem = (size_t)(kRowWarps / TEAM) * kWarpBuf * 8;
+  if (rnt_status s = ensure_attr(kern, smem, attr); s != RNT_OK) return s;
+  constexpr int rows_per_cta = (kRowWarps / TEAM) * (kWarpElems / P::Cn);
   const unsigned gx = (unsigned)((P::R + rows_per_cta - 1) / rows_per_cta);
   const uint64_t units = (uint64_t)batch * p->L;
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(gx, (unsigned)cnt);
-    k_rows<LOGN, MODE, LZ><<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
+    kern<<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -458,11 +467,11 @@ static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const
   if constexpr (MODE != 1) {
     // input from an LZ forward column pass (launch_col makes the same choice)
     if (p->lazy60 && lazy_enabled()) {
-      if (g_large_wide) return launch_rows_warp<LOGN, MODE, true>(p, out, in, bop, bcast, batch, st);
+      if (g_large_wide) return launch_rows_warp<LOGN, MODE, true, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
       return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC, true>(p, out, in, bop, bcast, batch, st);
     }
   }
-  if (g_large_wide) return launch_rows_warp<LOGN, MODE>(p, out, in, bop, bcast, batch, st);
+  if (g_large_wide) return launch_rows_warp<LOGN, MODE, false, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
@@ -470,7 +479,7 @@ template <int LOGN>
 static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in, const u64* bop, int bcast,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
-  g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= 192;
+  g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= RNT_WIDE_UNITS;
   switch (op) {
     case 0:  // forward
       if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;

@@ -467,23 +467,24 @@ k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict
 constexpr int kRowWarps = 2;
 constexpr int kRowKM = 3;
 
-template <int LOGN, int MODE, bool LZ = false>
+template <int LOGN, int MODE, bool LZ = false, int TEAM = 1>
 __global__ void __launch_bounds__(kRowWarps * 32, 12)
 k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_rows, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
   constexpr int n2 = P::n2;
   constexpr int N2 = P::Cn;
-  constexpr int RPW = kWarpElems / N2;   // rows per warp
+  constexpr int RPW = kWarpElems / N2;   // rows per warp buffer
+  static_assert(TEAM == 1 || TEAM == kRowWarps, "a team is one warp or the whole CTA");
   extern __shared__ __align__(16) u64 smem[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+  const int team = (int)(threadIdx.x >> 5) / TEAM;
+  const int lane = (int)threadIdx.x % (32 * TEAM);
   const uint64_t y = y0 + blockIdx.y;
   const uint32_t l = (uint32_t)(y / B);
   const uint64_t u = (y % B) * L + l;
-  const int r0 = (blockIdx.x * kRowWarps + warp) * RPW;
+  const int r0 = (blockIdx.x * (kRowWarps / TEAM) + team) * RPW;
   if (r0 >= P::R) return;
-  u64* buf = smem + (size_t)warp * kWarpBuf;
+  u64* buf = smem + (size_t)team * kWarpBuf;
   const u64 q = lc[l].q, q2 = lc[l].q2;
   const size_t base = u * (size_t)(P::R * P::Cn);
   const GView src{in + base, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
@@ -493,15 +494,15 @@ k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   const TW* Tm = Tr + (size_t)(P::R - 1 - r0) * N2;     // mirrored row R-1-r0 (- p * N2)
   const TW none{0, 0};
   if constexpr (MODE == 0) {
-    warp_forward<n2, kRowKM, kToGlobal, false, N2, LZ, P::n1>(buf, src, dst, lane, Tf, q, q2);
+    warp_forward<n2, kRowKM, kToGlobal, false, N2, LZ, P::n1, kFromGlobal, TEAM>(buf, src, dst, lane, Tf, q, q2);
   } else if constexpr (MODE == 1) {
-    warp_inverse<n2, kRowKM, false, false, N2, true>(buf, src, dst, lane, Tm, none, none, q, q2);
+    warp_inverse<n2, kRowKM, false, false, N2, true, false, kFromGlobal, TEAM>(buf, src, dst, lane, Tm, none, none, q,
+                                                                              q2);
   } else {
     const size_t boff = b_bcast ? (size_t)l * P::R * P::Cn : base;
     const GView bview{bop + boff, (uint64_t)r0, (uint64_t)N2, (uint64_t)P::R};
-    warp_polymul<n2, kRowKM, kFromGlobal, false, false, N2, true, LZ, P::n1>(buf, src, dst, bview, nullptr, lane, Tf, Tm,
-                                                                             none,
-                                                                  none, q, q2, lc[l].qinv);
+    warp_polymul<n2, kRowKM, kFromGlobal, false, false, N2, true, LZ, P::n1, kFromGlobal, TEAM>(
+        buf, src, dst, bview, nullptr, lane, Tf, Tm, none, none, q, q2, lc[l].qinv);
   }
 }
 
