@@ -67,7 +67,7 @@ WORKLOADS = {
 }
 
 L2_FLUSH_BYTES = 512 << 20   # >= 4x the 126 MB L2 (SURVEY §8(d) timing protocol)
-SPIN_CYCLES = 100_000   # ~50 us at 1.965 GHz
+SPIN_CYCLES = 400_000   # ~200 us at 1.965 GHz: absorbs host jitter before the start event
 FMA_SLOTS_PER_BFLY = 16   # exact Shoup butterfly: 6 wide/hi multiplies x 2 + 4 IMAD
 IMAD_SLOTS_PER_CLK_SM = 64
 N_SM = 148
@@ -127,7 +127,7 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period: float = 0.0):
+    def __init__(self, index: int, period: float = 0.001):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -663,7 +663,7 @@ def bench_ours(args, wl, parts):
             "data": "synthetic (seeded SplitMix64 uniform residues mod 60-bit NTT primes)",
             "config": {"workload": f"{wl}: {WORKLOADS[wl]['desc']}",
                        "l2": f"flushed ({L2_FLUSH_BYTES >> 20} MiB write) between steps, outside the timed events",
-                       "launch": "a ~50 us device spin precedes each step's start event (outside the events): "
+                       "launch": "a ~200 us device spin precedes each step's start event (outside the events): "
                                  "the events time device execution, not host launch latency",
                        "global_polys_per_part": [p[2] * (ws if args.scaling == 'weak' else 1) for p in parts],
                        "parallelism": (f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws} "

@@ -912,6 +912,17 @@ rnt_status rnt_plan_create(rnt_plan* out, uint32_t log2n, uint32_t n_limbs, cons
   const uint32_t n1 = (log2n + 1) / 2;
   const bool large = log2n > 10;
 
+  // The coefficient-form polymul (op 3) takes its NTT(b) temporary from the device's
+  // default stream-ordered pool (cudaMallocAsync); keep freed blocks in the pool instead
+  // of returning them to the driver at every synchronisation, so repeated calls reuse
+  // one allocation (the pool is per device; PyTorch's caching allocator does not use it).
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   p->lazy60 = true;
   for (uint32_t l = 0; l < n_limbs; ++l) p->lazy60 = p->lazy60 && limbs[l].q < (1ull << 60);
   std::vector<LimbC> lc(n_limbs);
