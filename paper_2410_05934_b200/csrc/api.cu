@@ -286,16 +286,24 @@ static bool lazy_enabled() {
 #ifndef RNT_WARP_MINB
 #define RNT_WARP_MINB 12
 #endif
-// Team size by batch (N = 2^10 polymul units): a CTA of 2 warps per polynomial
-// when the job fills fewer than RNT_TEAM2_WAVES waves of one-warp units
-// (experiments: -DRNT_TEAM2_WAVES=x; 0 disables).  Measured (profiles/r02/teams):
-// cfg2 (1.15 waves) 0.0816 -> 0.0764 ms, cfg5 (4.6 waves) 0.2619 -> 0.2609 ms;
-// teams of 4 warps: cfg2 0.0763, cfg5 0.2673 ms (not built).
+// N = 2^10 polymul units run on teams of 2 warps per polynomial (one CTA), compiled for
+// 16 CTAs = 32 warps per SM (<= 64 registers, no spills).  Measured (profiles/r02/teams,
+// team2_minb): one warp per polynomial at 24 warps/SM: cfg2 0.0816 ms, cfg5 k_warp 0.2619 ms
+// (cfg2's 4096 units are 1.15 waves); 2-warp teams at 24 warps/SM: 0.0764 / 0.2609; at 28 /
+// 32 / 36 / 40 / 48 warps/SM: cfg5 0.2594 / 0.2553 / 0.2565 / 0.2573 / 0.2653 ms, cfg2 0.0742
+// / 0.0741 / 0.0753 / 0.0766 / 0.0810 ms; teams of 4 warps: cfg2 0.0763, cfg5 0.2673 ms.
+// Experiment builds: -DRNT_TEAM2_WAVES=x (one-warp units from x waves up; default: always
+// teams), -DRNT_TEAM2_MINB=n.
 #ifndef RNT_TEAM2_WAVES
-#define RNT_TEAM2_WAVES 8
+#define RNT_TEAM2_WAVES 1e30
 #endif
 #ifndef RNT_TEAM2_MINB
-#define RNT_TEAM2_MINB RNT_WARP_MINB
+#define RNT_TEAM2_MINB 16
+#endif
+// Pass schedule of the LZ warp engine (Passes<LOGN, KM>): 32 = radix-8 with the split
+// tail (N = 2^10: 3 + 3 + 2 + 2); experiment builds: -DRNT_WARP_KM=40 (4 + 4 + 2).
+#ifndef RNT_WARP_KM
+#define RNT_WARP_KM 32
 #endif
 
 template <int LOGN, int MODE>
@@ -309,9 +317,10 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
     if constexpr (LOGN == 10 && MODE == 2) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
       if (waves < RNT_TEAM2_WAVES)
-        return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, 32, true, 2>(p, out, in, bop, bcast, batch, st);
+        return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, RNT_WARP_KM, true, 2>(p, out, in, bop, bcast, batch,
+                                                                                          st);
     }
-    return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 32, true>(p, out, in, bop, bcast, batch, st);
+    return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, RNT_WARP_KM, true>(p, out, in, bop, bcast, batch, st);
   }
   return launch_warp_v<LOGN, MODE, 2, RNT_WARP_MINB, false, 3>(p, out, in, bop, bcast, batch, st);
 }

@@ -1,0 +1,14 @@
+# cfg2 wave fit: 2-warp teams compiled for 12 / 14 / 16 CTAs per SM
+set -x
+O=gpurun_out/r02m; mkdir -p $O
+build() { RNT_NVCC_EXTRA="$1" python -c "from paper_2410_05934_b200 import build as b; b.build(force=True)" > $O/build_$2.txt 2>&1; }
+for m in 16 18 20 24; do
+  build "-DRNT_TEAM2_MINB=$m" $m
+  for w in cfg2 cfg5; do python bench.py --workload $w --steps 40 --no-cpu-baseline --no-e2e --no-graph > $O/bench_${w}_m$m.json 2>&1; done
+done
+build "" def
+python -c "
+import json,glob
+for f in sorted(glob.glob('$O/bench_cfg*.json')):
+    d=json.loads(open(f).read().strip().splitlines()[-1]); print(f.split('/')[-1], round(d['value']/1e6,3), round(d['ms_per_step'],4), round(d['roofline']['frac'],3), [round(p['ms'],4) for p in d['parts']], d.get('digests_ok'))
+"
