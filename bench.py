@@ -630,9 +630,13 @@ def bench_ours(args, wl, parts):
             traffic = json.load(open(prof)).get(f"{wl}:part{dom}")
         except Exception:
             traffic = None
-    kern = f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes)" \
-        if s["logn"] <= 10 else \
-        f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
+    if s["limbs"] * s["polys"] <= 2:
+        kern = f"k_clat / k_cluster <{s['logn']}> (single-launch cluster latency kernel)"
+    elif s["logn"] <= 10:
+        kern = (f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes, "
+                "2-warp teams, 32 warps/SM)")
+    else:
+        kern = f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
     # whole step: every butterfly of every part over the timed step time (all ranks)
     step_bfly = sum(2 * st["limbs"] * st["polys"] * (1 << st["logn"]) // 2 * st["logn"] for st in states) * (
         ws if args.scaling == "weak" else 1)

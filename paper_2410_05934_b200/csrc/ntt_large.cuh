@@ -467,8 +467,11 @@ k_row_mac(u64* __restrict__ uo, const u64* __restrict__ E, const u64* __restrict
 constexpr int kRowWarps = 2;
 constexpr int kRowKM = 3;
 
+#ifndef RNT_ROWS_MINB
+#define RNT_ROWS_MINB 12
+#endif
 template <int LOGN, int MODE, bool LZ = false, int TEAM = 1>
-__global__ void __launch_bounds__(kRowWarps * 32, 12)
+__global__ void __launch_bounds__(kRowWarps * 32, RNT_ROWS_MINB)
 k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
        const TW* __restrict__ tw_rows, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   using P = TwoPass<LOGN>;
