@@ -394,6 +394,7 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // 0.827 -> 0.804 ms); smaller jobs the 16-column tiles and k_row (k_rows
 // under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
 static thread_local bool g_large_wide = false;   // set by large_op for the current call
+static thread_local bool g_rows_warp = false;    // rows through k_rows (wide path or RNT_ROWS_WARP_UNITS)
 // Experiment builds: -DRNT_WIDE_UNITS=n (limb-units from which the wide path is taken),
 // -DRNT_ROWS_TEAM=2 (k_rows with 2-warp teams).
 #ifndef RNT_WIDE_UNITS
@@ -401,6 +402,9 @@ static thread_local bool g_large_wide = false;   // set by large_op for the curr
 #endif
 #ifndef RNT_ROWS_TEAM
 #define RNT_ROWS_TEAM 1
+#endif
+#ifndef RNT_ROWS_WARP_UNITS
+#define RNT_ROWS_WARP_UNITS RNT_WIDE_UNITS
 #endif
 
 template <int LOGN, int CT, bool LZ = false>
@@ -476,11 +480,11 @@ static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const
   if constexpr (MODE != 1) {
     // input from an LZ forward column pass (launch_col makes the same choice)
     if (p->lazy60 && lazy_enabled()) {
-      if (g_large_wide) return launch_rows_warp<LOGN, MODE, true, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
+      if (g_rows_warp) return launch_rows_warp<LOGN, MODE, true, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
       return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC, true>(p, out, in, bop, bcast, batch, st);
     }
   }
-  if (g_large_wide) return launch_rows_warp<LOGN, MODE, false, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
+  if (g_rows_warp) return launch_rows_warp<LOGN, MODE, false, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
   return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
 }
 
@@ -489,6 +493,7 @@ static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in,
                            uint32_t batch, cudaStream_t st) {
   rnt_status s;
   g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= RNT_WIDE_UNITS;
+  g_rows_warp = g_large_wide || (LOGN == 16 && (uint64_t)batch * p->L >= RNT_ROWS_WARP_UNITS);
   switch (op) {
     case 0:  // forward
       if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
