@@ -395,6 +395,7 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
 // under-fills the GPU for one 45-limb polynomial: cfg3 0.097 -> 0.111 ms).
 static thread_local bool g_large_wide = false;   // set by large_op for the current call
 static thread_local bool g_rows_warp = false;    // rows through k_rows (wide path or RNT_ROWS_WARP_UNITS)
+static thread_local bool g_col8 = false;         // 8-column pass-1 tiles (wide path or RNT_COL8_UNITS)
 // Experiment builds: -DRNT_WIDE_UNITS=n (limb-units from which the wide path is taken),
 // -DRNT_ROWS_TEAM=2 (k_rows with 2-warp teams).
 #ifndef RNT_WIDE_UNITS
@@ -405,6 +406,9 @@ static thread_local bool g_rows_warp = false;    // rows through k_rows (wide pa
 #endif
 #ifndef RNT_ROWS_WARP_UNITS
 #define RNT_ROWS_WARP_UNITS RNT_WIDE_UNITS
+#endif
+#ifndef RNT_COL8_UNITS
+#define RNT_COL8_UNITS RNT_WIDE_UNITS
 #endif
 
 template <int LOGN, int CT, bool LZ = false>
@@ -431,10 +435,10 @@ static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64*
   // forward columns with lazy CT ranges when the plan allows it; the row pass
   // that consumes them (launch_row) makes the same choice
   if (!inv && p->lazy60 && lazy_enabled()) {
-    if (g_large_wide) return launch_col_v<LOGN, 8, true>(p, inv, after_mont, out, in, batch, st);
+    if (g_col8) return launch_col_v<LOGN, 8, true>(p, inv, after_mont, out, in, batch, st);
     return launch_col_v<LOGN, kColTile, true>(p, inv, after_mont, out, in, batch, st);
   }
-  if (g_large_wide) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
+  if (g_col8) return launch_col_v<LOGN, 8>(p, inv, after_mont, out, in, batch, st);
   return launch_col_v<LOGN, kColTile>(p, inv, after_mont, out, in, batch, st);
 }
 
@@ -494,6 +498,7 @@ static rnt_status large_op(const rnt_plan_s* p, int op, u64* out, const u64* in,
   rnt_status s;
   g_large_wide = LOGN == 16 && (uint64_t)batch * p->L >= RNT_WIDE_UNITS;
   g_rows_warp = g_large_wide || (LOGN == 16 && (uint64_t)batch * p->L >= RNT_ROWS_WARP_UNITS);
+  g_col8 = g_large_wide || (LOGN == 16 && (uint64_t)batch * p->L >= RNT_COL8_UNITS);
   switch (op) {
     case 0:  // forward
       if ((s = launch_col<LOGN>(p, false, 0, out, in, batch, st)) != RNT_OK) return s;
