@@ -309,10 +309,11 @@ static bool lazy_enabled() {
 template <int LOGN, int MODE>
 static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop,
                               int bcast, uint32_t batch, cudaStream_t st) {
-  // radix-8 passes, 2 warps per CTA, <= 85 registers (24 warps/SM) -- fastest measured
-  // (profiles/r01/README.md); lazy CT ranges with the split-tail schedule (N = 2^10:
-  // 3 + 3 + 2 + 2, the polymul turn pass on 4-coefficient groups) when every modulus is
-  // below 2^60; [0, 4q) Harvey ranges with 3 + 3 + 3 + 1 otherwise
+  // radix-8 passes, 2 warps per CTA: one warp per buffer at <= 85 registers (24 warps/SM),
+  // or for the N = 2^10 polymul a 2-warp team per buffer at <= 64 registers (32 warps/SM);
+  // lazy CT ranges with the split-tail schedule (N = 2^10: 3 + 3 + 2 + 2, the polymul turn
+  // pass on 4-coefficient groups) when every modulus is below 2^60; [0, 4q) Harvey ranges
+  // with 3 + 3 + 3 + 1 otherwise
   if (p->lazy60 && lazy_enabled()) {
     if constexpr (LOGN == 10 && MODE == 2) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
