@@ -720,3 +720,29 @@ print("EXT_OK" if ok else "EXT_BAD")
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=600)
     assert "EXT_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("ws", [3, 8])
+def test_sharded_cfg5_on_one_gpu_matches_golden(ws):
+    """SURVEY §4.2 T5 on one GPU: the exact ws-way strong split of cfg5 that
+    `bench.py --gpus ws` runs (bench.plan_blocks: limb x polynomial shards, inputs
+    from global counters), every shard computed by the CUDA path in turn; the
+    concatenated per-unit digests equal the oracle's golden hash for the whole job."""
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("rnt_bench_t5", os.path.join(root, "bench.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
+    parts = B.WORKLOADS["cfg5"]["parts"]
+    rows = []
+    for rank in range(ws):
+        for blk in B.plan_blocks(parts, ws, rank, "strong"):
+            a, bh = B.block_inputs(blk)
+            p = R.Plan(blk["logn"], blk["mods"])
+            c = empty_dev(a.shape)
+            R.polymul(p, c, to_dev(a), to_dev(bh), b_is_eval=True)
+            rows += B.block_digests(blk, from_dev(c))
+            p.destroy()
+    assert B.check_digests("cfg5", rows) is True
