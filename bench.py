@@ -1191,6 +1191,11 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
+    ap.add_argument("--log2n", type=int, default=None,
+                    help="custom workload instead of a preset: N = 2^log2n (with --limbs, --batch, --seed)")
+    ap.add_argument("--limbs", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="strong (default): the fixed workload split over the ranks; weak: N copies")
@@ -1223,6 +1228,12 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours" and not single:
         # one process per GPU: re-launch this script under torch.distributed.run
         sys.exit(relaunch(args.gpus, sys.argv[1:]))
+    if args.log2n is not None:
+        # a custom single-part workload (reading-C2 primes); no golden digests (digests_ok: null)
+        WORKLOADS["custom"] = {"desc": f"N=2^{args.log2n}, {args.limbs} limbs x {args.batch} polynomials, "
+                                       f"seed {args.seed}, NTT -> (.) b_hat -> INTT",
+                               "parts": [(args.log2n, args.limbs, args.batch, args.seed)]}
+        args.workload = "custom"
     if args.launch_check:
         return launch_check(args)
     wl = args.workload
