@@ -286,8 +286,8 @@ static bool lazy_enabled() {
 #ifndef RNT_WARP_MINB
 #define RNT_WARP_MINB 12
 #endif
-// N = 2^10 polymul units run on teams of 2 warps per polynomial (one CTA), compiled for
-// 16 CTAs = 32 warps per SM (<= 64 registers, no spills).  Measured (profiles/r02/teams,
+// N = 2^10 units (forward, inverse, polymul) run on teams of 2 warps per polynomial (one
+// CTA), compiled for 16 CTAs = 32 warps per SM (<= 64 registers, no spills).  Measured (profiles/r02/teams,
 // team2_minb): one warp per polynomial at 24 warps/SM: cfg2 0.0816 ms, cfg5 k_warp 0.2619 ms
 // (cfg2's 4096 units are 1.15 waves); 2-warp teams at 24 warps/SM: 0.0764 / 0.2609; at 28 /
 // 32 / 36 / 40 / 48 warps/SM: cfg5 0.2594 / 0.2553 / 0.2565 / 0.2573 / 0.2653 ms, cfg2 0.0742
@@ -315,7 +315,7 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   // pass on 4-coefficient groups) when every modulus is below 2^60; [0, 4q) Harvey ranges
   // with 3 + 3 + 3 + 1 otherwise
   if (p->lazy60 && lazy_enabled()) {
-    if constexpr (LOGN == 10 && MODE == 2) {
+    if constexpr (LOGN == 10) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
       if (waves < RNT_TEAM2_WAVES)
         return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, RNT_WARP_KM, true, 2>(p, out, in, bop, bcast, batch,
