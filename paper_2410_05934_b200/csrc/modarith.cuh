@@ -173,4 +173,15 @@ __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 q, u64 qinv) {
   return hi - mh + q;           // (a b - m q) / 2^64 + q in (0, 2q)
 }
 
+// T 2^{-64} mod q for an exact sum of products T < 15 q 2^64 (Montgomery
+// reduction of the whole sum): (T - m q) / 2^64 + q = hi - hi64(m q) + q in
+// (0, 16q) with m q == T mod 2^64; three conditional subtractions -> [0, 2q).
+// Callers are LZ kernels (q < 2^60, 16q < 2^64).
+__device__ __forceinline__ u64 redc_sum(unsigned __int128 T, u64 q, u64 q2, u64 qinv) {
+  const u64 lo = (u64)T, hi = (u64)(T >> 64);
+  const u64 m = lo * qinv;
+  const u64 r = hi - __umul64hi(m, q) + q;   // (0, 16q)
+  return csub(csub(csub(r, q2 << 2), q2 << 1), q2);
+}
+
 }  // namespace rnt

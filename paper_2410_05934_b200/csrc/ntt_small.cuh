@@ -640,13 +640,26 @@ k_extprod_cta(u64* __restrict__ out, const u64* __restrict__ c, const u64* __res
     for (int r = 0; r < NW; ++r) {   // all loads first: one latency for the whole sum
       z0[r] = __ldg(zhat + (size_t)(2 * r) * N + k);
       z1[r] = __ldg(zhat + (size_t)(2 * r + 1) * N + k);
-      x[r] = smem[(size_t)r * kWarpBuf + pe];   // lazy [0, 4q)
+      x[r] = smem[(size_t)r * kWarpBuf + pe];   // lazy: [0, 15q) (LZ) or [0, 4q)
     }
     u64 a0 = 0, a1 = 0;
+    if constexpr (LZ) {
+      // exact 128-bit sums, one Montgomery reduction per output instead of one per
+      // product: x < 15q (LZ forward output), z < q, NW <= 16 -> T < 240 q^2 < 15 q 2^64
+      unsigned __int128 T0 = 0, T1 = 0;
 #pragma unroll
-    for (int r = 0; r < NW; ++r) {
-      a0 = csub(a0 + mont_mul(x[r], z0[r], q, qinv), q2);
-      a1 = csub(a1 + mont_mul(x[r], z1[r], q, qinv), q2);
+      for (int r = 0; r < NW; ++r) {
+        T0 += (unsigned __int128)x[r] * z0[r];
+        T1 += (unsigned __int128)x[r] * z1[r];
+      }
+      a0 = redc_sum(T0, q, q2, qinv);
+      a1 = redc_sum(T1, q, q2, qinv);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NW; ++r) {
+        a0 = csub(a0 + mont_mul(x[r], z0[r], q, qinv), q2);
+        a1 = csub(a1 + mont_mul(x[r], z1[r], q, qinv), q2);
+      }
     }
     smem[pe] = a0;
     smem[kWarpBuf + pe] = a1;
