@@ -166,8 +166,10 @@ __device__ __forceinline__ u64 canon16(u64 x, u64 q, u64 q2) {
 __device__ __forceinline__ u64 canon2(u64 x, u64 q) { return csub(x, q); }
 
 __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 q, u64 qinv) {
-  u64 lo = a * b;
-  u64 hi = __umul64hi(a, b);
+  // one 128-bit product (4 IMAD.WIDE) instead of lo and hi separately (5 + 2 IMAD)
+  const unsigned __int128 T = (unsigned __int128)a * b;
+  u64 lo = (u64)T;
+  u64 hi = (u64)(T >> 64);
   u64 m = lo * qinv;            // m q == lo (mod 2^64)
   u64 mh = __umul64hi(m, q);
   return hi - mh + q;           // (a b - m q) / 2^64 + q in (0, 2q)
