@@ -112,58 +112,57 @@ __global__ void k_pointwise(u64* __restrict__ c, const u64* __restrict__ a, cons
 // Galois automorphism sigma_g (rnt_automorph).
 //   NTT form:  out[k] = in[pi(k)],  2 brv(pi(k)) + 1 = (2 brv(k) + 1) g mod 2N
 //   coeff form: out[j] = +-in[j g^{-1} mod 2N] (sign when the source index >= N)
-// Scatter formulation: a thread reads in[e] (coalesced) and writes it to its destination --
-// pi^{-1} is the same map with g^{-1}, and coefficient i goes to i g mod 2N (negated past
-// N) -- so the loads never stall on a gather.  In NTT form pi maps every aligned block of
-// 32 slots onto one aligned block of 32 slots (the 5 low bits of k are the high bits of
-// brv(k), and multiplying by odd g mod 2N permutes high bits among themselves), so a
-// warp's 32 scattered 8-byte stores still cover whole 32-byte sectors of one 256-byte run.
-// Each thread loads KA pairs of slots with 16-byte loads, all in flight before the
-// first store (the one-element grid-stride loop was latency bound on small jobs:
-// cfg3 moves 47 MB at 0.43 of HBM).
-constexpr int kAutoPairs = 4;
-__device__ __forceinline__ void automorph_put(u64* __restrict__ out, const LimbC* __restrict__ lc, uint64_t e, u64 x,
-                                              uint32_t L, uint32_t logn, uint32_t g, uint32_t ginv, int ntt_domain) {
+// Scatter formulation (default): a thread reads in[e] (coalesced) and writes it to its
+// destination -- pi^{-1} is the same map with g^{-1}, and coefficient i goes to i g mod
+// 2N (negated past N) -- so the loads never stall on a gather; the 8-byte scattered
+// stores merge into sectors in L2.  RNT_AUTOMORPH_SCATTER=0 (experiment builds) keeps the
+// gather form.  One limb is 8N bytes (512 KB at 2^16): L2-resident while it is permuted.
+#ifndef RNT_AUTOMORPH_SCATTER
+#define RNT_AUTOMORPH_SCATTER 1
+#endif
+__global__ void k_automorph(u64* __restrict__ out, const u64* __restrict__ in, const LimbC* __restrict__ lc,
+                            uint32_t L, uint32_t logn, uint32_t g, uint32_t ginv, int ntt_domain, uint64_t total) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t n = 1u << logn, mask2n = 2 * n - 1;
-  const uint64_t u = e >> logn;
-  const uint32_t k = (uint32_t)(e & (n - 1));
-  u64* dst = out + (u << logn);
-  if (ntt_domain) {
-    const uint32_t ek = 2u * (__brev(k) >> (32 - logn)) + 1u;
-    const uint32_t es = (uint32_t)(((uint64_t)ek * ginv) & mask2n);
-    __stcs(dst + (__brev((es - 1u) >> 1) >> (32 - logn)), x);
-  } else {
-    const uint32_t t = (uint32_t)(((uint64_t)k * g) & mask2n);
-    if (t < n) {
-      __stcs(dst + t, x);
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint64_t u = e >> logn;
+    const uint32_t k = (uint32_t)(e & (n - 1));
+#if RNT_AUTOMORPH_SCATTER
+    const u64 x = __ldcs(in + e);
+    u64* dst = out + (u << logn);
+    if (ntt_domain) {
+      const uint32_t ek = 2u * (__brev(k) >> (32 - logn)) + 1u;
+      const uint32_t es = (uint32_t)(((uint64_t)ek * ginv) & mask2n);
+      dst[__brev((es - 1u) >> 1) >> (32 - logn)] = x;
     } else {
-      const u64 q = lc[u % L].q;
-      __stcs(dst + (t - n), x ? q - x : 0ull);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) k_automorph(u64* __restrict__ out, const u64* __restrict__ in,
-                                                   const LimbC* __restrict__ lc, uint32_t L, uint32_t logn, uint32_t g,
-                                                   uint32_t ginv, int ntt_domain, uint64_t total) {
-  const uint64_t npair = total >> 1;   // total = units N, N >= 16: even
-  const ulonglong2* in2 = reinterpret_cast<const ulonglong2*>(in);
-  const uint64_t step = (uint64_t)gridDim.x * blockDim.x * kAutoPairs;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x * kAutoPairs + threadIdx.x; b < npair; b += step) {
-    ulonglong2 v[kAutoPairs];
-#pragma unroll
-    for (int i = 0; i < kAutoPairs; ++i) {
-      const uint64_t p = b + (uint64_t)i * blockDim.x;
-      if (p < npair) v[i] = __ldcs(in2 + p);
-    }
-#pragma unroll
-    for (int i = 0; i < kAutoPairs; ++i) {
-      const uint64_t p = b + (uint64_t)i * blockDim.x;
-      if (p < npair) {
-        automorph_put(out, lc, 2 * p, v[i].x, L, logn, g, ginv, ntt_domain);
-        automorph_put(out, lc, 2 * p + 1, v[i].y, L, logn, g, ginv, ntt_domain);
+      const uint32_t t = (uint32_t)(((uint64_t)k * g) & mask2n);
+      if (t < n) {
+        dst[t] = x;
+      } else {
+        const u64 q = lc[u % L].q;
+        dst[t - n] = x ? q - x : 0ull;
       }
     }
+#else
+    const u64* src = in + (u << logn);
+    u64 v;
+    if (ntt_domain) {
+      const uint32_t ek = 2u * (__brev(k) >> (32 - logn)) + 1u;          // odd exponent of slot k
+      const uint32_t es = (uint32_t)(((uint64_t)ek * g) & mask2n);       // times g mod 2N (odd)
+      const uint32_t kk = __brev((es - 1u) >> 1) >> (32 - logn);
+      v = __ldg(src + kk);
+    } else {
+      const uint32_t i0 = (uint32_t)(((uint64_t)k * ginv) & mask2n);
+      if (i0 < n) {
+        v = __ldg(src + i0);
+      } else {
+        const u64 x = __ldg(src + (i0 - n));
+        const u64 q = lc[u % L].q;
+        v = x ? q - x : 0ull;
+      }
+    }
+    out[e] = v;
+#endif
   }
 }
 
@@ -1163,8 +1162,8 @@ rnt_status rnt_automorph(rnt_plan p, uint64_t* out, const uint64_t* in, uint32_t
   }
   const uint64_t total = (uint64_t)batch * p->L << p->logn;
   const int threads = 256;
-  uint64_t blocks = (total / 2 + threads * kAutoPairs - 1) / (threads * kAutoPairs);
-  const uint64_t cap = (uint64_t)num_sms() * 8;
+  uint64_t blocks = (total + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   k_automorph<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<u64*>(out), reinterpret_cast<const u64*>(in), p->d_lc, p->L, p->logn, galois_elt, ginv,
@@ -1536,19 +1535,21 @@ rnt_status rnt_execute_host(rnt_plan p, rnt_op op, uint64_t* out_host, const uin
   // Chunking: chunks over polynomials (batch > 1) or limbs (batch == 1),
   // round-robin over three internal streams so H2D copy, kernels and D2H copy
   // of successive chunks overlap.  Fork/join with the caller's stream by events.
-  // chunk bytes: 16 MiB (measured best of 4 .. 64)
+  // Chunks of 32 MiB, uniform (round 2 sweep, profiles/r02/e2e: 32 MiB uniform beats the
+  // earlier 16 MiB chunks with a ramp by 11 % on cfg5, 16 % on cfg2, 12 % on cfg3 and
+  // 23 % on the serial schedule -- in a stream of calls the ramp's small chunks only
+  // add per-copy overhead; RNT_EXPERIMENTS builds: RNT_E2E_CHUNK_MB, RNT_E2E_RAMP).
 #ifdef RNT_EXPERIMENTS
-  const size_t target = (size_t)(getenv("RNT_E2E_CHUNK_MB") ? atoi(getenv("RNT_E2E_CHUNK_MB")) : 16) << 20;
+  const size_t target = (size_t)(getenv("RNT_E2E_CHUNK_MB") ? atoi(getenv("RNT_E2E_CHUNK_MB")) : 32) << 20;
 #else
-  constexpr size_t target = (size_t)16 << 20;
+  constexpr size_t target = (size_t)32 << 20;
 #endif
   // Granule = one polynomial (batch > 1) or one limb (batch == 1).  Chunks of
-  // `target` bytes, except that the first and last chunks ramp (target/8,
-  // /4, /2, ...) so the copy engines start and drain sooner (measured better than uniform).
+  // `target` bytes; with `ramp` the first and last chunks ramp (target/8, /4, /2, ...).
 #ifdef RNT_EXPERIMENTS
-  const bool ramp = !getenv("RNT_E2E_NORAMP");
+  const bool ramp = getenv("RNT_E2E_RAMP") != nullptr;
 #else
-  constexpr bool ramp = true;
+  constexpr bool ramp = false;
 #endif
   const size_t gbytes = batch > 1 ? (size_t)p->L * unit_bytes : unit_bytes;
   const size_t G = batch > 1 ? batch : p->L;
