@@ -431,7 +431,8 @@ def bench_ours(args, wl, parts):
         streams = run_streams if streams is None else streams
         if span is not None:
             span[0].record(base)
-        for i, s in enumerate(states):
+        order = list(enumerate(states))
+        for i, s in (order[::-1] if args.reverse_parts else order):
             rs = streams[i]
             if rs is not base:
                 rs.wait_stream(base)
@@ -1220,6 +1221,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
     ap.add_argument("--e2e-serial", dest="e2e_overlap", action="store_false",
                     help="e2e: join every step before the next (default: consecutive steps stream)")
+    ap.add_argument("--reverse-parts", action="store_true",
+                    help="launch the parts of a step in reverse order (experiment: cfg5 k_warp first)")
     ap.add_argument("--sequential-parts", dest="concurrent_parts", action="store_false",
                     help="run the parts of a step one after another on one stream (default: concurrent)")
     ap.add_argument("--concurrent-parts", dest="concurrent_parts", action="store_true",

@@ -1082,7 +1082,11 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   // better).  The window streams belong to the plan, so concurrent callers of one
   // plan serialise on them; a stream under CUDA-graph capture skips the split (the
   // plan's streams must not join another thread's capture).
+#ifdef RNT_EXPERIMENTS
+  static const int split_g = env_int("RNT_SPLIT_G", 2) < 1 ? 1 : (env_int("RNT_SPLIT_G", 2) > 4 ? 4 : env_int("RNT_SPLIT_G", 2));
+#else
   constexpr int split_g = 2;
+#endif
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   RNT_CUDA(cudaStreamIsCapturing(st, &cap));
   if (cap == cudaStreamCaptureStatusNone && batch == 1 && p->L >= (uint32_t)(2 * split_g) && !p->is_view) {
