@@ -321,11 +321,13 @@ def test_binding_rejects_undersized_or_mistyped_buffers():
         R.execute_host(p, R.OP_FORWARD, torch.zeros((2, 2, 1024), dtype=torch.int64), hin, a)   # host out too small
 
 
-@pytest.mark.parametrize("logn,limbs,batch,op", [(10, 1, 4096, "fwd"), (10, 2, 1500, "polymul_eval"),
-                                                 (16, 45, 1, "polymul_eval"), (16, 9, 3, "inv"),
-                                                 (16, 12, 1, "polymul")])
+# Shapes above the 32 MiB chunk: (10,1,10000) 3 chunks over polynomials (4096, 4096, 1808),
+# (10,2,5000) 3 (2048, 2048, 904), (16,70,1) 2 limb windows (64 + 6), (16,9,9) 2 (7 + 2).
+@pytest.mark.parametrize("logn,limbs,batch,op", [(10, 1, 10000, "fwd"), (10, 2, 5000, "polymul_eval"),
+                                                 (16, 70, 1, "polymul_eval"), (16, 9, 9, "inv"),
+                                                 (16, 70, 1, "polymul"), (16, 45, 1, "polymul_eval")])
 def test_execute_host_chunked_pipeline(logn, limbs, batch, op):
-    """rnt_execute_host splits large jobs into chunks over 3 internal streams."""
+    """rnt_execute_host splits large jobs into 32 MiB chunks over 3 internal streams."""
     ps, psi = params(logn, limbs)
     p = R.Plan(logn, ps)
     a = inputs.residues(12, batch, ps, 1 << logn)
