@@ -625,10 +625,14 @@ def bench_ours(args, wl, parts):
     dom_ms = statistics.mean(part_ms_seq[dom])   # rank 0's dominant kernel
     achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
     traffic = None
+    sass = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{wl}:part{dom}")
+            tj = json.load(open(prof))
+            traffic = tj.get(f"{wl}:part{dom}")
+            if states[dom]["logn"] == 10 and states[dom]["limbs"] * states[dom]["polys"] > 512:
+                sass = tj.get("sass:k_warp<10,2>")
         except Exception:
             traffic = None
     if s["limbs"] * s["polys"] <= 2:
@@ -652,6 +656,7 @@ def bench_ours(args, wl, parts):
             "incl_pointwise_basis": f"x {pw_factor:.3f}: + 1.5 butterfly-equivalents per coefficient for the "
                                     "Montgomery (.) and + 1 per last-stage butterfly for the N^-1 product",
             "step_achieved_per_gpu": step_achieved, "step_frac": step_achieved / peak_bfly,
+            "sass_per_butterfly": sass,
             "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
                           f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
     parts_out = []
