@@ -288,7 +288,7 @@ def bench_reference(args, wl, parts):
 GOLDEN_DIGESTS = os.path.join(ROOT, "tests", "golden", "bench_digests.json")
 
 
-def plan_blocks(parts, ws: int, rank: int, scaling: str):
+def plan_blocks(parts, ws: int, rank: int, scaling: str, planner: str = "contig"):
     """The blocks of the global job that `rank` owns.
 
     strong: the fixed workload is split by limb x polynomial with the weighted
@@ -306,7 +306,7 @@ def plan_blocks(parts, ws: int, rank: int, scaling: str):
                             poff=rank * polys, seed=seed))
     else:
         sp = [shd.Part(lg, lm, po) for (lg, lm, po, _) in parts]
-        for b in shd.plan(sp, ws)[rank]:
+        for b in shd.PLANNERS[planner](sp, ws)[rank]:
             logn, limbs, polys, seed = parts[b.part]
             out.append(dict(part=b.part, logn=logn, mods=primes_for(logn, limbs)[b.limb_begin:b.limb_end],
                             loff=b.limb_begin, ltot=limbs, polys=b.poly_end - b.poly_begin, poff=b.poly_begin,
@@ -378,6 +378,10 @@ def bench_ours(args, wl, parts):
     import paper_2410_05934_b200 as R
 
     ws, rank, local = dist_env()
+    # --emulate-rank R (testing): one process times rank R's shard of a --gpus N plan
+    plan_ws, plan_rank = ws, rank
+    if args.emulate_rank is not None:
+        plan_ws, plan_rank = args.gpus, args.emulate_rank
     ndev = torch.cuda.device_count()
     # RNT_BENCH_SHARE_GPU=1 (testing the multi-rank path on a 1-GPU box only): ranks
     # share the visible GPUs and talk over gloo; never used for a reported number
@@ -400,7 +404,7 @@ def bench_ours(args, wl, parts):
 
     # ---- shard (plan_blocks): strong = the fixed workload split by limb x polynomial,
     # weak = rank r owns polynomial block r of ws copies
-    blocks = plan_blocks(parts, ws, rank, args.scaling)
+    blocks = plan_blocks(parts, plan_ws, plan_rank, args.scaling, args.shard)
     states = []
     for blk in blocks:
         a, bhat = block_inputs(blk)
@@ -586,7 +590,8 @@ def bench_ours(args, wl, parts):
     for st in states:
         rows += block_digests(st["blk"], st["c"].cpu().numpy().view(np.uint64))
     all_rows = gather_rows(rows, ws)
-    digests_ok = check_digests(wl, all_rows) if (args.scaling == "strong" or ws == 1) else None
+    digests_ok = (check_digests(wl, all_rows) if (args.scaling == "strong" or ws == 1) else None) \
+        if args.emulate_rank is None else None
     e2e_match = None
     if args.e2e:   # the host-buffer path returned the same outputs as the device path
         last = (args.steps - 1) % 2 if args.e2e_overlap else 0
@@ -1180,7 +1185,7 @@ def launch_check(args):
         dist.init_process_group("gloo")
     parts = WORKLOADS[args.workload]["parts"]
     rows = []
-    for blk in plan_blocks(parts, ws, rank, args.scaling):
+    for blk in plan_blocks(parts, ws, rank, args.scaling, args.shard):
         a, _ = block_inputs(blk)
         rows += block_digests(blk, a)
     all_rows = gather_rows(rows, ws)
@@ -1226,6 +1231,12 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-buffer phase (profiling)")
     ap.add_argument("--e2e-serial", dest="e2e_overlap", action="store_false",
                     help="e2e: join every step before the next (default: consecutive steps stream)")
+    ap.add_argument("--shard", default="parts", choices=["contig", "mixed", "parts"],
+                    help="strong-scaling shard planner (shard.py): whole ranks per part when world >= 2 x parts, "
+                         "else the contiguous weighted split (parts, default); contig; every rank a slice of "
+                         "every part (mixed)")
+    ap.add_argument("--emulate-rank", type=int, default=None,
+                    help="testing: one process times rank R's shard of the --gpus N plan (no process group)")
     ap.add_argument("--reverse-parts", action="store_true",
                     help="launch the parts of a step in reverse order (experiment: cfg5 k_warp first)")
     ap.add_argument("--sequential-parts", dest="concurrent_parts", action="store_false",
@@ -1244,7 +1255,8 @@ def main():
     if args.scaling is None:
         args.scaling = "strong"
     single = args.latency or args.automorph or args.extprod or args.modup or args.keyswitch or args.hrf
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours" and not single:
+    if (args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours" and not single
+            and args.emulate_rank is None):
         # one process per GPU: re-launch this script under torch.distributed.run
         sys.exit(relaunch(args.gpus, sys.argv[1:]))
     if args.log2n is not None:

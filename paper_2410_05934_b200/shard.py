@@ -70,6 +70,81 @@ def plan(parts: list[Part], world: int) -> list[list[Block]]:
     return [_merge(s) for s in shards]
 
 
+def plan_mixed(parts: list[Part], world: int) -> list[list[Block]]:
+    """Every rank gets a slice of every part (cfg5: ~45/world limbs of the 2^16
+    polynomial and ~16384/world of the 2^10 batch), so each rank runs the same mix
+    as one GPU does and its parts overlap on two streams.  The parts with coarse
+    units are split evenly by unit count (a rank's share differs by at most one
+    unit); the part with the finest units then fills every rank up to the mean
+    weight, which evens out the coarse parts' rounding."""
+    if world < 1:
+        raise ValueError("world >= 1")
+    shards: list[list[Block]] = [[] for _ in range(world)]
+    load = [0] * world
+    order = sorted(range(len(parts)), key=lambda i: -parts[i].weight)
+    fine = order[-1]
+
+    def units_to_blocks(pi, u0, u1):
+        """Units [u0, u1) of part pi (limb-major: unit = l * polys + b) as rectangles."""
+        p = parts[pi]
+        out = []
+        u = u0
+        while u < u1:
+            l, b = divmod(u, p.polys)
+            nb = min(p.polys - b, u1 - u)
+            out.append(Block(pi, l, l + 1, b, b + nb))
+            u += nb
+        return out
+
+    for pi in order[:-1]:
+        p = parts[pi]
+        n = p.limbs * p.polys
+        for r in range(world):
+            u0, u1 = n * r // world, n * (r + 1) // world
+            shards[r] += units_to_blocks(pi, u0, u1)
+            load[r] += (u1 - u0) * p.weight
+    p = parts[fine]
+    n = p.limbs * p.polys
+    total = sum(load) + n * p.weight
+    u = 0
+    for r in range(world):
+        # fine units for rank r: fill up to the cumulative target (last rank takes the rest)
+        target = total * (r + 1) // world - sum(load[: r + 1]) - u * p.weight
+        k = n - u if r == world - 1 else max(0, min(n - u, round(target / p.weight)))
+        shards[r] += units_to_blocks(fine, u, u + k)
+        u += k
+    return [_merge(s) for s in shards]
+
+
+def plan_by_part(parts: list[Part], world: int) -> list[list[Block]]:
+    """Whole ranks per part: part p gets k_p ranks, k_p proportional to its weight
+    (largest remainder, at least one each), and its units are split contiguously
+    among them -- so no rank runs two kernel chains and pays both parts' fixed
+    costs (launch ramps and tails dominate a rank's step at 8 GPUs: one 2^16 x 45
+    chain costs ~36 us before its first limb, the 2^10 batch ~18 us).  Needs
+    world >= 2 x parts, else the contiguous split (plan)."""
+    if world < 2 * len(parts):
+        return plan(parts, world)
+    w = [p.weight * p.limbs * p.polys for p in parts]
+    total = sum(w)
+    k = [max(1, int(world * x // total)) for x in w]
+    while sum(k) < world:   # largest remainder
+        i = max(range(len(parts)), key=lambda j: world * w[j] / total - k[j])
+        k[i] += 1
+    while sum(k) > world:
+        i = max(range(len(parts)), key=lambda j: k[j] - world * w[j] / total if k[j] > 1 else -1e9)
+        k[i] -= 1
+    shards: list[list[Block]] = []
+    for pi, p in enumerate(parts):
+        sub = plan([p], k[pi])
+        for sh in sub:
+            shards.append([Block(pi, b.limb_begin, b.limb_end, b.poly_begin, b.poly_end) for b in sh])
+    return shards
+
+
+PLANNERS = {"contig": plan, "mixed": plan_mixed, "parts": plan_by_part}
+
+
 def _merge(blocks: list[Block]) -> list[Block]:
     """Merge consecutive single-limb blocks with identical poly ranges."""
     out: list[Block] = []
@@ -88,8 +163,8 @@ def shard_weight(parts: list[Part], shard: list[Block]) -> int:
     return sum(parts[b.part].weight * b.units for b in shard)
 
 
-def efficiency(parts: list[Part], world: int) -> float:
+def efficiency(parts: list[Part], world: int, planner: str = "contig") -> float:
     """Ideal parallel efficiency of the split: mean shard weight / max."""
-    sh = plan(parts, world)
+    sh = PLANNERS[planner](parts, world)
     ws = [shard_weight(parts, s) for s in sh]
     return (sum(ws) / world) / max(ws)

@@ -58,9 +58,11 @@ def _unit_digests(parts, blocks, seed_base=0):
     return out
 
 
-def test_plan_covers_every_unit_once():
-    for world in (1, 2, 3, 4, 8):
-        sh = S.plan(PARTS, world)
+@pytest.mark.parametrize("planner", ["contig", "mixed", "parts"])
+def test_plan_covers_every_unit_once(planner):
+    for world in (1, 2, 3, 4, 5, 8):
+        sh = S.PLANNERS[planner](PARTS, world)
+        assert len(sh) == world
         seen = {}
         for r, blocks in enumerate(sh):
             for b in blocks:
@@ -71,6 +73,17 @@ def test_plan_covers_every_unit_once():
                         seen[key] = r
         want = {(pi, l, pb) for pi, p in enumerate(PARTS) for l in range(p.limbs) for pb in range(p.polys)}
         assert set(seen) == want
+
+
+def test_plan_by_part_gives_whole_ranks_per_part():
+    cfg5 = [S.Part(16, 45, 1), S.Part(10, 1, 16384)]
+    sh = S.plan_by_part(cfg5, 8)
+    parts_of = [{b.part for b in s} for s in sh]
+    assert all(len(p) == 1 for p in parts_of)                      # no rank runs both chains
+    assert [next(iter(p)) for p in parts_of].count(0) == 2          # 2 of 8 ranks take the 2^16 part
+    assert sorted(sum(b.units for b in s) for s in sh[:2]) == [22, 23]
+    assert S.plan_by_part(cfg5, 3) == S.plan(cfg5, 3)              # fewer than 2 ranks per part: contiguous
+    assert S.plan_by_part([S.Part(10, 1, 4096)], 8) == S.plan([S.Part(10, 1, 4096)], 8)
 
 
 def test_plan_balance_matches_survey_table():
@@ -207,6 +220,21 @@ def test_bench_relaunch_command():
     assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
     assert "--nproc-per-node=8" in cmd and "127.0.0.1" in cmd
     assert cmd[-3:] == ["--gpus", "8", "--steps", "3"][-3:] and cmd[-4] == "--gpus"
+
+
+@pytest.mark.timeout(300)
+def test_bench_gpus4_launcher_gloo_parts_planner():
+    """`bench.py --gpus 4` (strong, default planner: whole ranks per part) over gloo:
+    every unit of cfg5 planned exactly once and the gathered digests match."""
+    import json
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--launch-check",
+                        "--workload", "cfg5"], capture_output=True, text=True, timeout=280, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["n_gpus"] == 4 and d["digests_match"] is True and d["units"] == 45 + 16384
 
 
 @pytest.mark.timeout(300)
