@@ -532,33 +532,40 @@ def bench_ours(args, wl, parts):
     # ---- secondary: the step captured once in a CUDA graph and replayed (no host
     # launch work per step), L2 flushed between replays like the timed region
     graph = None
-    if args.graph and states:
-        try:
-            g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream()
-            cap.wait_stream(stream)
-            gstreams = [torch.cuda.Stream() for _ in states] if concurrent else [cap for _ in states]
-            with torch.cuda.stream(cap):
-                with torch.cuda.graph(g, stream=cap):
-                    step(None, None, gstreams, base=cap)
-            stream.wait_stream(cap)
-            gspans = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(min(args.steps, 50))]
-            barrier()
+    if args.graph:
+        # every rank takes part in the two barriers (a rank with an empty shard, or whose
+        # capture failed, only waits), so the collectives stay matched across ranks
+        g = None
+        if states:
+            try:
+                g = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream()
+                cap.wait_stream(stream)
+                gstreams = [torch.cuda.Stream() for _ in states] if concurrent else [cap for _ in states]
+                with torch.cuda.stream(cap):
+                    with torch.cuda.graph(g, stream=cap):
+                        step(None, None, gstreams, base=cap)
+                stream.wait_stream(cap)
+            except Exception as e:   # capture is an optional measurement; report why it is absent
+                graph = {"error": f"{type(e).__name__}: {e}"[:200]}
+                g = None
+        gspans = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(min(args.steps, 50))]
+        barrier()
+        if g is not None:
             for sp in gspans:
                 flush.zero_()
                 torch.cuda._sleep(SPIN_CYCLES)
                 sp[0].record(stream)
                 g.replay()
                 sp[1].record(stream)
-            barrier()
+        barrier()
+        if g is not None:
             gms = [sp[0].elapsed_time(sp[1]) for sp in gspans]
             local_xf = sum(2 * st["limbs"] * st["polys"] for st in states)
             graph = {"ms_per_step": statistics.mean(gms), "median": statistics.median(gms),
                      "rank0_value": local_xf / (statistics.mean(gms) * 1e-3), "unit": UNIT,
                      "note": "secondary, rank 0: one step captured in a CUDA graph, replayed; L2 flushed"}
             del g
-        except Exception as e:   # capture is an optional measurement; report why it is absent
-            graph = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- end to end through the C ABI with host buffers (pinned), H2D + D2H inside
     e2e_ms = float("nan")
@@ -625,45 +632,47 @@ def bench_ours(args, wl, parts):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     peak_bfly = N_SM * IMAD_SLOTS_PER_CLK_SM / FMA_SLOTS_PER_BFLY * f_max / 1e9   # Gbfly/s
-    s = states[dom]
-    bfly_launch = 2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]
-    dom_ms = statistics.mean(part_ms_seq[dom])   # rank 0's dominant kernel
-    achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    sass = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            tj = json.load(open(prof))
-            traffic = tj.get(f"{wl}:part{dom}")
-            if states[dom]["logn"] == 10 and states[dom]["limbs"] * states[dom]["polys"] > 512:
-                sass = tj.get("sass:k_warp<10,2>")
-        except Exception:
-            traffic = None
-    if s["limbs"] * s["polys"] <= 2:
-        kern = f"k_clat / k_cluster <{s['logn']}> (single-launch cluster latency kernel)"
-    elif s["logn"] <= 10:
-        kern = (f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes, "
-                "2-warp teams, 32 warps/SM)")
-    else:
-        kern = f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
-    # whole step: every butterfly of every part over the timed step time (all ranks)
-    step_bfly = sum(2 * st["limbs"] * st["polys"] * (1 << st["logn"]) // 2 * st["logn"] for st in states) * (
-        ws if args.scaling == "weak" else 1)
-    step_achieved = step_bfly * args.steps / (total_ms * 1e-3) / 1e9 / ws
-    # the polymul's other multiplies in butterfly equivalents (16 IMAD slots each): the
-    # Montgomery (.) per coefficient (24 slots = 1.5) and the second Shoup product of the
-    # last inverse stage's N/2 butterflies (N^-1 on both outputs, 1 each): 2N per unit
-    pw_factor = 1.0 + 2.0 / s["logn"]
-    roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak_bfly,
-            "unit": "Gbutterfly/s", "frac": achieved / peak_bfly, "traffic": traffic,
-            "frac_incl_pointwise": achieved * pw_factor / peak_bfly,
-            "incl_pointwise_basis": f"x {pw_factor:.3f}: + 1.5 butterfly-equivalents per coefficient for the "
-                                    "Montgomery (.) and + 1 per last-stage butterfly for the N^-1 product",
-            "step_achieved_per_gpu": step_achieved, "step_frac": step_achieved / peak_bfly,
-            "sass_per_butterfly": sass,
-            "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
-                          f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
+    roof = None   # a rank with an empty shard (more ranks than units) only times and reports nothing
+    if states:
+        s = states[dom]
+        bfly_launch = 2 * s["limbs"] * s["polys"] * (1 << s["logn"]) // 2 * s["logn"]
+        dom_ms = statistics.mean(part_ms_seq[dom])   # rank 0's dominant kernel
+        achieved = bfly_launch / (dom_ms * 1e-3) / 1e9
+        traffic = None
+        sass = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                tj = json.load(open(prof))
+                traffic = tj.get(f"{wl}:part{dom}")
+                if states[dom]["logn"] == 10 and states[dom]["limbs"] * states[dom]["polys"] > 512:
+                    sass = tj.get("sass:k_warp<10,2>")
+            except Exception:
+                traffic = None
+        if s["limbs"] * s["polys"] <= 2:
+            kern = f"k_clat / k_cluster <{s['logn']}> (single-launch cluster latency kernel)"
+        elif s["logn"] <= 10:
+            kern = (f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes, "
+                    "2-warp teams, 32 warps/SM)")
+        else:
+            kern = f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
+        # whole step: every butterfly of every part over the timed step time (all ranks)
+        step_bfly = sum(2 * st["limbs"] * st["polys"] * (1 << st["logn"]) // 2 * st["logn"] for st in states) * (
+            ws if args.scaling == "weak" else 1)
+        step_achieved = step_bfly * args.steps / (total_ms * 1e-3) / 1e9 / ws
+        # the polymul's other multiplies in butterfly equivalents (16 IMAD slots each): the
+        # Montgomery (.) per coefficient (24 slots = 1.5) and the second Shoup product of the
+        # last inverse stage's N/2 butterflies (N^-1 on both outputs, 1 each): 2N per unit
+        pw_factor = 1.0 + 2.0 / s["logn"]
+        roof = {"bound": "alu", "kernel": kern, "achieved": achieved, "peak": peak_bfly,
+                "unit": "Gbutterfly/s", "frac": achieved / peak_bfly, "traffic": traffic,
+                "frac_incl_pointwise": achieved * pw_factor / peak_bfly,
+                "incl_pointwise_basis": f"x {pw_factor:.3f}: + 1.5 butterfly-equivalents per coefficient for the "
+                                        "Montgomery (.) and + 1 per last-stage butterfly for the N^-1 product",
+                "step_achieved_per_gpu": step_achieved, "step_frac": step_achieved / peak_bfly,
+                "sass_per_butterfly": sass,
+                "peak_basis": f"{N_SM} SMs x {IMAD_SLOTS_PER_CLK_SM} IMAD slots/clk / {FMA_SLOTS_PER_BFLY} slots "
+                              f"per exact-Shoup butterfly x {f_max/1e6:.0f} MHz (sm_max_mhz)"}
     parts_out = []
     for i, st in enumerate(states):
         ms = statistics.mean(part_ms_seq[i])
@@ -689,7 +698,7 @@ def bench_ours(args, wl, parts):
                                  "the events time device execution, not host launch latency",
                        "global_polys_per_part": [p[2] * (ws if args.scaling == 'weak' else 1) for p in parts],
                        "parallelism": (f"{'batch' if args.scaling == 'weak' else 'limb/batch'}-sharded x{ws} "
-                                       f"({'N copies of the workload' if args.scaling == 'weak' else 'the fixed workload split by shard.plan'}), "
+                                       f"({'N copies of the workload' if args.scaling == 'weak' else 'the fixed workload split by shard planner ' + args.shard}), "
                                        "no data-path collective")},
             "gpus_active": gpus_active,
             "process_group": backend if ws > 1 else None,
