@@ -9,6 +9,7 @@
 #include <atomic>
 #include <mutex>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -1083,7 +1084,7 @@ static rnt_status run_op(rnt_plan p, int op, uint64_t* out_, const uint64_t* in_
   // plan serialise on them; a stream under CUDA-graph capture skips the split (the
   // plan's streams must not join another thread's capture).
 #ifdef RNT_EXPERIMENTS
-  static const int split_g = env_int("RNT_SPLIT_G", 2) < 1 ? 1 : (env_int("RNT_SPLIT_G", 2) > 4 ? 4 : env_int("RNT_SPLIT_G", 2));
+  static const int split_g = std::min(4, std::max(1, env_int("RNT_SPLIT_G", 2)));   // limb windows
 #else
   constexpr int split_g = 2;
 #endif
