@@ -413,6 +413,24 @@ static thread_local bool g_col8 = false;         // 8-column pass-1 tiles (wide 
 #define RNT_COL8_UNITS RNT_WIDE_UNITS
 #endif
 
+// Launch with the programmatic-stream-serialization attribute: the kernel may be
+// scheduled before its stream predecessor finishes and waits for it in-kernel (pdl_wait,
+// ntt_large.cuh).  Used for the dependent kernels of an N >= 2^11 chain.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = RNT_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <int LOGN, int CT, bool LZ = false>
 static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u64* out, const u64* in,
                                uint32_t batch, cudaStream_t st) {
@@ -421,9 +439,10 @@ static rnt_status launch_col_v(const rnt_plan_s* p, bool inv, int after_mont, u6
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(P::Cn / CT, (unsigned)cnt);
-    if (inv)
-      k_col_inv<LOGN, CT><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_inv, p->d_lc, p->L, batch, y0, after_mont);
-    else
+    if (inv) {
+      RNT_CUDA(launch_pdl(k_col_inv<LOGN, CT>, g, dim3(CT * P::T1), 0, st, out, in, p->d_col_inv, p->d_lc, p->L,
+                          batch, y0, after_mont));
+    } else
       k_col_fwd<LOGN, CT, false, LZ><<<g, CT * P::T1, 0, st>>>(out, in, p->d_col_fwd, p->d_lc, p->L, batch, y0);
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
@@ -452,7 +471,8 @@ static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, con
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(P::R / RPC_, (unsigned)cnt);
-    k_row<LOGN, MODE, RPC_, LZ><<<g, RPC_ * P::T2, 0, st>>>(out, in, bop, bcast, p->d_fwd, p->d_lc, p->L, batch, y0);
+    RNT_CUDA(launch_pdl(k_row<LOGN, MODE, RPC_, LZ>, g, dim3(RPC_ * P::T2), 0, st, out, in, bop, bcast, p->d_fwd,
+                        p->d_lc, p->L, batch, y0));
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }
@@ -473,7 +493,8 @@ static rnt_status launch_rows_warp(const rnt_plan_s* p, u64* out, const u64* in,
   for (uint64_t y0 = 0; y0 < units; y0 += 65535u) {
     const uint64_t cnt = units - y0 < 65535u ? units - y0 : 65535u;
     dim3 g(gx, (unsigned)cnt);
-    kern<<<g, kRowWarps * 32, smem, st>>>(out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L, batch, y0);
+    RNT_CUDA(launch_pdl(kern, g, dim3(kRowWarps * 32), smem, st, out, in, bop, bcast, p->d_rowtw, p->d_lc, p->L,
+                        batch, y0));
     rnt_status s = after_launch();
     if (s != RNT_OK) return s;
   }

@@ -25,6 +25,33 @@
 
 namespace rnt {
 
+// Programmatic dependent launch between the kernels of one N >= 2^11 chain (column ->
+// row -> column pass, api.cu launch_pdl): the dependent is launched with the programmatic
+// serialization attribute, so its launch overlaps the primary's last CTAs (the implicit
+// trigger at CTA exit), and it waits for the primary's completion and memory before its
+// first read of the primary's output (pdl_wait; a no-op for a launch without the
+// attribute).  Measured (profiles/r02/pdl): cfg3 90.8 -> 89.4 us, cfg5 336.6 -> 334.4 us,
+// cfg4 745.9 -> 740.8 us, a 23-limb 2^16 polymul (the 8-GPU shard) 65.5 -> 60.0 us.  An
+// explicit trigger at kernel entry (RNT_PDL_EARLY=1: dependents resident early, waiting)
+// was slower for the two-window chains (cfg3 99-100 us): waiting CTAs hold slots the other
+// window needs.
+#ifndef RNT_PDL
+#define RNT_PDL 1
+#endif
+#ifndef RNT_PDL_EARLY
+#define RNT_PDL_EARLY 0
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if RNT_PDL && RNT_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if RNT_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 constexpr int kEl = 16;       // coefficients per thread
 constexpr int kColTile = 16;  // columns per pass-1 CTA (one 128-byte line per row)
 
@@ -134,6 +161,7 @@ __global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
 k_col_fwd(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   __shared__ __align__(16) u64 tile[TwoPass<LOGN>::R * CT];
+  if constexpr (!MODUP) pdl_trigger();
   col_fwd_tile<LOGN, CT, MODUP, LZ>(out, in, tw_col, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, tile);
 }
 
@@ -192,6 +220,7 @@ __global__ void RNT_COL_BOUNDS(CT * TwoPass<LOGN>::T1)
 k_col_inv(u64* __restrict__ out, const u64* __restrict__ in, const TW* __restrict__ tw_col,
           const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0, int after_mont) {
   __shared__ __align__(16) u64 tile[TwoPass<LOGN>::R * CT];
+  pdl_wait();
   col_inv_tile<LOGN, CT>(out, in, tw_col, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, after_mont, tile);
 }
 
@@ -365,6 +394,8 @@ __global__ void RNT_ROW_BOUNDS(RPC_ * TwoPass<LOGN>::T2)
 k_row(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict__ bop, int b_bcast,
       const TW* __restrict__ tw_row_fwd, const LimbC* __restrict__ lc, uint32_t L, uint32_t B, uint64_t y0) {
   __shared__ __align__(16) u64 sbuf[RPC_ * TwoPass<LOGN>::ROWBUF];
+  pdl_trigger();
+  pdl_wait();
   row_tile<LOGN, MODE, RPC_, LZ>(out, in, bop, b_bcast, tw_row_fwd, lc, L, B, y0 + blockIdx.y, (int)blockIdx.x, sbuf);
 }
 
@@ -480,6 +511,8 @@ k_rows(u64* __restrict__ out, const u64* __restrict__ in, const u64* __restrict_
   constexpr int RPW = kWarpElems / N2;   // rows per warp buffer
   static_assert(TEAM == 1 || TEAM == kRowWarps, "a team is one warp or the whole CTA");
   extern __shared__ __align__(16) u64 smem[];
+  pdl_trigger();
+  pdl_wait();
   const int team = (int)(threadIdx.x >> 5) / TEAM;
   const int lane = (int)threadIdx.x % (32 * TEAM);
   const uint64_t y = y0 + blockIdx.y;

@@ -1,0 +1,15 @@
+# programmatic dependent launch in the N >= 2^11 chain: parity + cfg3 / cfg4 / cfg5 / 22-limb shard
+O=gpurun_out/pdl; mkdir -p $O
+cp exp/lib_pdl1.so paper_2410_05934_b200/librnsntt.so
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "16 or 13 or 11 or large or cfg or cluster or execute or split or window or graph" > $O/pytest.txt 2>&1; tail -2 $O/pytest.txt
+for r in 1 2; do for v in pdl0 pdl1; do
+  cp exp/lib_$v.so paper_2410_05934_b200/librnsntt.so
+  line="$v run$r:"
+  for w in cfg3 cfg5 cfg4; do
+    python bench.py --workload $w --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > $O/${v}_${w}_$r.json 2>&1
+    line="$line $w:$(tail -1 $O/${v}_${w}_$r.json | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"]*1000,1), round(d["cuda_graph"]["ms_per_step"]*1000,1) if "ms_per_step" in (d.get("cuda_graph") or {}) else d.get("cuda_graph"), d["digests_ok"])')"
+  done
+  python bench.py --log2n 16 --limbs 23 --batch 1 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-graph > $O/${v}_L23_$r.json 2>&1
+  echo "$line L23:$(tail -1 $O/${v}_L23_$r.json | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"]*1000,1))')"
+done; done
+cp exp/lib_pdl1.so paper_2410_05934_b200/librnsntt.so
