@@ -318,6 +318,13 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
   if (p->lazy60 && lazy_enabled()) {
     if constexpr (LOGN == 10) {
       const double waves = (double)batch * p->L / ((double)num_sms() * RNT_WARP_MINB * 2);
+      // below 3 waves of 2-warp teams, teams of 4 warps (8 CTAs = 32 warps per SM): a shorter
+      // critical path per polynomial beats the coarser wave quantization (round 2, session 3,
+      // profiles/r02/t4: 1200 / 2731 / 3000 / 4096 / 6000 polymuls 37.1 / 61.1 / 65.0 / 78.6 /
+      // 108.7 -> 34.9 / 57.1 / 61.9 / 77.7 / 107.4 us; 8192 / 16384: 139.5 / 259.1 -> 140.6 /
+      // 262.3 us, so larger batches keep the 2-warp teams)
+      if ((uint64_t)batch * p->L < (uint64_t)num_sms() * RNT_TEAM2_MINB * 3)
+        return launch_warp_v<LOGN, MODE, 4, 8, false, RNT_WARP_KM, true, 4>(p, out, in, bop, bcast, batch, st);
       if (waves < RNT_TEAM2_WAVES)
         return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, RNT_WARP_KM, true, 2>(p, out, in, bop, bcast, batch,
                                                                                           st);
