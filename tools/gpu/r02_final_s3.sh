@@ -1,6 +1,6 @@
 # round-2 evidence: every bench line, launch list, ncu full of the dominant kernels, sanitizer, tests
 set -x
-O=gpurun_out/r02s3; mkdir -p $O /tmp/r02z
+O=gpurun_out/r02s4; mkdir -p $O /tmp/r02z
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/smi.txt
 lscpu | head -20 > $O/lscpu.txt
 timeout 1800 python -m pytest tests -m gpu -q --timeout 900 > $O/pytest_gpu.txt 2>&1; tail -3 $O/pytest_gpu.txt
