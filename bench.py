@@ -652,8 +652,9 @@ def bench_ours(args, wl, parts):
         if s["limbs"] * s["polys"] <= 2:
             kern = f"k_clat / k_cluster <{s['logn']}> (single-launch cluster latency kernel)"
         elif s["logn"] <= 10:
+            team = "4-warp" if s["logn"] == 10 and s["limbs"] * s["polys"] < 3 * N_SM * 16 else "2-warp"
             kern = (f"k_warp<{s['logn']},2> (fused NTT->(.)->INTT, one launch; lazy CT ranges, 3+3+2+2 passes, "
-                    "2-warp teams, 32 warps/SM)")
+                    f"{team} teams, 32 warps/SM)")
         else:
             kern = f"k_col_fwd<{s['logn']}> + k_row<{s['logn']},2> + k_col_inv<{s['logn']}> (polymul, 3 launches)"
         # whole step: every butterfly of every part over the timed step time (all ranks)
