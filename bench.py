@@ -645,7 +645,7 @@ def bench_ours(args, wl, parts):
             try:
                 tj = json.load(open(prof))
                 traffic = tj.get(f"{wl}:part{dom}")
-                if states[dom]["logn"] == 10 and states[dom]["limbs"] * states[dom]["polys"] > 512:
+                if states[dom]["logn"] == 10 and states[dom]["limbs"] * states[dom]["polys"] >= 3 * N_SM * 16:
                     sass = tj.get("sass:k_warp<10,2>")
             except Exception:
                 traffic = None
