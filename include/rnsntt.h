@@ -62,7 +62,8 @@ typedef enum {
 /* Dispatch test hooks (read once per process; defaults are the shipped
  * behaviour, the hooks exist so tests can reach every kernel instantiation):
  *   RNT_LAT_UNITS=k      N <= 2^10 jobs of <= k (poly, limb) units use the
- *                        latency engine k_lat (default 512; 0 = never);
+ *                        latency engine k_lat (default 512; 256 for N = 2^10 with
+ *                        every q < 2^60; 0 = never);
  *   RNT_CLUSTER_UNITS=k  jobs of <= k units use the single-launch cluster
  *                        kernels (default 2; 0 = never);
  *   RNT_LAZY=0           keep the [0, 4q) kernels even when every q < 2^60;

@@ -336,11 +336,14 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
 
 // Latency engine (k_lat, ntt_small.cuh) for jobs of at most lat_units()
 // (polynomial, limb) units at N <= 2^10 (env RNT_LAT_UNITS; 0 disables).  Default
-// 512: measured crossover with the warp engine near 1024 units (2^10 polymul,
-// 18.6 vs 24.7 us at 512 units, 52.5 vs 46.6 us at 2048).
-static int lat_units() {
-  static const int v = env_int("RNT_LAT_UNITS", 512);
-  return v;
+// 512 (round 1: crossover with the warp engine near 1024 units, 2^10 polymul 18.6 vs
+// 24.7 us at 512 units), 256 for the N = 2^10 LZ plans whose warp engine runs 4-warp
+// teams on small batches (round 2, profiles/r02/lat: 128 / 256 / 384 / 512 units 16.6 /
+// 20.0 / 24.1 / 26.6 us on k_lat, 19.9 / 20.0 / 21.7 / 22.6 us on the warp engine).
+static int lat_units(const rnt_plan_s* p) {
+  static const int v = env_int("RNT_LAT_UNITS", -1);
+  if (v >= 0) return v;
+  return (p->logn == 10 && p->lazy60 && lazy_enabled()) ? 256 : 512;
 }
 
 template <int LOGN, int MODE>
@@ -382,7 +385,7 @@ static rnt_status warp_dispatch(const rnt_plan_s* p, u64* out, const u64* in, co
     if (p->logn == 10 && (uint64_t)batch * p->L <= (uint64_t)cluster_units() && clat_enabled())
       return clat_op<10>(p, MODE, out, in, bop, bcast, batch, st);
   }
-  if ((uint64_t)batch * p->L <= (uint64_t)lat_units()) return lat_dispatch<MODE>(p, out, in, bop, bcast, batch, st);
+  if ((uint64_t)batch * p->L <= (uint64_t)lat_units(p)) return lat_dispatch<MODE>(p, out, in, bop, bcast, batch, st);
   switch (p->logn) {
     case 4: return launch_warp<4, MODE>(p, out, in, bop, bcast, batch, st);
     case 5: return launch_warp<5, MODE>(p, out, in, bop, bcast, batch, st);
