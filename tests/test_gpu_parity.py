@@ -412,6 +412,33 @@ def test_latency_path(logn, limbs, batch, op):
     assert np.array_equal(from_dev(d), want)
 
 
+# N = 2^10 launch shapes by job size (api.cu launch_warp / lat_units): <= 256 units the
+# latency engine, below 3 x 148 x 16 units 4-warp teams, above 2-warp teams -- every mode
+# on each shape, ragged batch sizes
+@pytest.mark.parametrize("batch", [200, 300, 7200])
+@pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_coeff_bcast"])
+def test_n1024_launch_shapes(batch, op):
+    ps, psi = params(10, 1)
+    p = R.Plan(10, ps)
+    a = inputs.residues(61, batch, ps, 1024)
+    d = empty_dev(a.shape)
+    if op == "fwd":
+        R.ntt_forward(p, d, to_dev(a))
+        want = O.batch(O.OP_FWD, a, ps, psi, n_threads=8)
+    elif op == "inv":
+        R.ntt_inverse(p, d, to_dev(a))
+        want = O.batch(O.OP_INV, a, ps, psi, n_threads=8)
+    elif op == "polymul_eval":
+        b = inputs.residues(62, batch, ps, 1024)
+        R.polymul(p, d, to_dev(a), to_dev(O.batch(O.OP_FWD, b, ps, psi, n_threads=8)), b_is_eval=True)
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, n_threads=8)
+    else:
+        b = inputs.residues(63, 1, ps, 1024)
+        R.polymul(p, d, to_dev(a), to_dev(b), b_is_eval=False, b_broadcast=True)
+        want = O.batch(O.OP_POLYMUL, a, ps, psi, b=b, b_broadcast=True, n_threads=8)
+    assert np.array_equal(from_dev(d), want)
+
+
 @pytest.mark.parametrize("logn", [10, 11, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("limbs,batch", [(1, 1), (2, 1), (1, 2)])
 @pytest.mark.parametrize("op", ["fwd", "inv", "polymul_eval", "polymul_bcast"])
