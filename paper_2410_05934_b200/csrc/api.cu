@@ -473,6 +473,14 @@ static rnt_status launch_col(const rnt_plan_s* p, bool inv, int after_mont, u64*
   return launch_col_v<LOGN, kColTile>(p, inv, after_mont, out, in, batch, st);
 }
 
+// Rows per k_row CTA (experiment builds: -DRNT_ROW_RPC=n with -DRNT_ROW_MINB=m; 8 rows x 4
+// CTAs/SM measured within 0.5 % of the default 16 x 2, profiles/r02/README).
+#ifndef RNT_ROW_RPC
+#define RNT_ROW_RPC 0
+#endif
+template <int LOGN>
+constexpr int kRowRpc() { return RNT_ROW_RPC ? RNT_ROW_RPC : TwoPass<LOGN>::RPC; }
+
 template <int LOGN, int MODE, int RPC_, bool LZ = false>
 static rnt_status launch_row_v(const rnt_plan_s* p, u64* out, const u64* in, const u64* bop, int bcast,
                                uint32_t batch, cudaStream_t st) {
@@ -518,11 +526,11 @@ static rnt_status launch_row(const rnt_plan_s* p, u64* out, const u64* in, const
     // input from an LZ forward column pass (launch_col makes the same choice)
     if (p->lazy60 && lazy_enabled()) {
       if (g_rows_warp) return launch_rows_warp<LOGN, MODE, true, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
-      return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC, true>(p, out, in, bop, bcast, batch, st);
+      return launch_row_v<LOGN, MODE, kRowRpc<LOGN>(), true>(p, out, in, bop, bcast, batch, st);
     }
   }
   if (g_rows_warp) return launch_rows_warp<LOGN, MODE, false, RNT_ROWS_TEAM>(p, out, in, bop, bcast, batch, st);
-  return launch_row_v<LOGN, MODE, TwoPass<LOGN>::RPC>(p, out, in, bop, bcast, batch, st);
+  return launch_row_v<LOGN, MODE, kRowRpc<LOGN>()>(p, out, in, bop, bcast, batch, st);
 }
 
 template <int LOGN>
