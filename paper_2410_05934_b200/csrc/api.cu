@@ -301,6 +301,11 @@ static bool lazy_enabled() {
 #ifndef RNT_TEAM2_MINB
 #define RNT_TEAM2_MINB 16
 #endif
+// Jobs below this many waves of 2-warp teams run 4-warp teams (experiment builds:
+// -DRNT_TEAM4_WAVES=x).
+#ifndef RNT_TEAM4_WAVES
+#define RNT_TEAM4_WAVES 3
+#endif
 // Pass schedule of the LZ warp engine (Passes<LOGN, KM>): 32 = radix-8 with the split
 // tail (N = 2^10: 3 + 3 + 2 + 2); experiment builds: -DRNT_WARP_KM=40 (4 + 4 + 2).
 #ifndef RNT_WARP_KM
@@ -323,7 +328,7 @@ static rnt_status launch_warp(const rnt_plan_s* p, u64* out, const u64* in, cons
       // profiles/r02/t4: 1200 / 2731 / 3000 / 4096 / 6000 polymuls 37.1 / 61.1 / 65.0 / 78.6 /
       // 108.7 -> 34.9 / 57.1 / 61.9 / 77.7 / 107.4 us; 8192 / 16384: 139.5 / 259.1 -> 140.6 /
       // 262.3 us, so larger batches keep the 2-warp teams)
-      if ((uint64_t)batch * p->L < (uint64_t)num_sms() * RNT_TEAM2_MINB * 3)
+      if ((uint64_t)batch * p->L < (uint64_t)num_sms() * RNT_TEAM2_MINB * RNT_TEAM4_WAVES)
         return launch_warp_v<LOGN, MODE, 4, 8, false, RNT_WARP_KM, true, 4>(p, out, in, bop, bcast, batch, st);
       if (waves < RNT_TEAM2_WAVES)
         return launch_warp_v<LOGN, MODE, 2, RNT_TEAM2_MINB, false, RNT_WARP_KM, true, 2>(p, out, in, bop, bcast, batch,
